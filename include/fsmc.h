@@ -1,0 +1,173 @@
+/* fsmc.h -- C ABI of the B200 multi-chain FSM MCMC engine (libfsmc.so).
+ *
+ * This is the drop-in boundary for the reference's multi-chain sampling path
+ * (/root/reference/pkg/src/fsm_mcmc).  The reference is pure Python, so its
+ * "FFI" is the Python call surface; each entry point below replaces the
+ * reference function named beside it, and paper_2503_17405_b200/ is the
+ * Python host mirror that binds it with ctypes (INTEGRATION.md shows the
+ * stub a maintainer would add to the reference).
+ *
+ * Conventions: plain pointers and sizes only.  Every buffer is device memory
+ * allocated by the caller (torch tensors in the Python host) unless marked
+ * "host".  `stream` is a cudaStream_t passed as void*.  Entry points never
+ * throw; they return an fsmc_status and record a message retrievable with
+ * fsmc_last_error().  Launches are stream-ordered and never synchronise the
+ * device except where noted.  Arithmetic is IEEE fp64 (the reference's).
+ */
+#ifndef FSMC_H
+#define FSMC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSMC_ABI_VERSION 1
+#define FSMC_NINT 32        /* int64 slots per chain in fsmc_state.ints */
+#define FSMC_MAX_MODES 8    /* mixture components in FSMC_T_MOG */
+
+typedef enum {
+  FSMC_OK = 0,
+  FSMC_ERR_ARG = 1,          /* invalid argument (mirrors ValueError / KernelError) */
+  FSMC_ERR_CUDA = 2,         /* CUDA runtime failure */
+  FSMC_ERR_UNSUPPORTED = 3   /* configuration not compiled (dimension / lanes) */
+} fsmc_status;
+
+/* kernel families: drmh_kernel (kernels/drmh.py:63), elliptical_kernel
+ * (kernels/elliptical.py:65), nuts_kernel (kernels/nuts.py:103) */
+enum { FSMC_DRMH = 1, FSMC_ESS = 2, FSMC_NUTS = 3 };
+
+/* step variants, lockstep.py:44 STEP_VARIANTS */
+enum { FSMC_PLAIN = 0, FSMC_BUNDLED = 1, FSMC_AMORTIZED = 2 };
+
+/* device log-density plugins (TargetModel, targets.py:45-60) */
+enum {
+  FSMC_T_GAUSS_DIAG = 1,     /* gaussian_target with diagonal factor            targets.py:74 */
+  FSMC_T_GAUSS_DENSE = 2,    /* gaussian_target, dense L^-1 and precision       targets.py:100-114 */
+  FSMC_T_GAUSS_EQUICORR = 3, /* gaussian_target whose covariance is a*I + b*11^T (closed form) */
+  FSMC_T_MOG = 4,            /* correlated_mog_target                           targets.py:137 */
+  FSMC_T_FUNNEL = 5,         /* Neal's funnel (BASELINE config 2) */
+  FSMC_T_NANBAND = 6,        /* fault injection: std normal, `b` once x[0] > `a` */
+  FSMC_T_LOGISTIC = 7,       /* -sum log(1+exp(-y*x)): GP-classification latent (f-space) */
+  FSMC_T_FLAT = 8            /* log density 0 */
+};
+
+/* Gaussian-prior split for the elliptical kernel (targets.py:37-42) */
+enum { FSMC_PRIOR_NONE = 0, FSMC_PRIOR_IDENTITY = 1, FSMC_PRIOR_DENSE = 2 };
+
+typedef struct fsmc_kernel {
+  int32_t family;
+  int32_t max_tries;            /* drmh: M */
+  double proposal_scale;        /* drmh: proposal N(y, scale^2 I) */
+  double step_size;             /* nuts: epsilon */
+  int32_t max_depth;            /* nuts */
+  int32_t split_body;           /* reserved (drmh split body), must be 0 */
+  double divergence_threshold;  /* nuts */
+} fsmc_kernel;
+
+typedef struct fsmc_target {
+  int32_t kind;                 /* FSMC_T_* */
+  int32_t dim;
+  int32_t n_modes;              /* FSMC_T_MOG */
+  int32_t prior_kind;           /* FSMC_PRIOR_* (elliptical kernel only) */
+  double log_norm;              /* Gaussian / MoG normaliser, computed as the reference does */
+  double a, b;                  /* EQUICORR/MOG: 1/a_perp, 1/(a+d*b); FUNNEL: a = v scale;
+                                   NANBAND: a = threshold, b = value returned */
+  double pad;
+  double offsets[FSMC_MAX_MODES];  /* MOG mode offsets (mode k = offsets[k] * 1) */
+  const double* mean;           /* [dim] or NULL (zero mean) */
+  const double* diag;           /* [dim] GAUSS_DIAG: diagonal of L^-1 (dim 1: unused) */
+  const double* diag2;          /* [dim] GAUSS_DIAG: diagonal of the precision */
+  const double* mat_t;          /* [dim*dim] GAUSS_DENSE: (L^-1)^T row-major */
+  const double* mat2_t;         /* [dim*dim] GAUSS_DENSE: precision^T row-major */
+  const double* yvec;           /* [dim] LOGISTIC labels (+-1) */
+  const double* prior_t;        /* [dim*dim] PRIOR_DENSE: L^T row-major (L lower-triangular) */
+} fsmc_target;
+
+/* Per-chain structure-of-arrays state, allocated by the caller with the
+ * sizes fsmc_state_layout() reports.  Replaces ChainBatch + the *Locals
+ * records (lockstep.py:158-172, drmh.py:35, elliptical.py:32, nuts.py:64). */
+typedef struct fsmc_state {
+  int64_t m;                    /* chains in this state block */
+  int64_t dim;
+  int32_t n_vec;                /* vectors per chain */
+  int32_t n_scal;               /* fp64 scalars per chain */
+  double* vec;                  /* [m][n_vec][dim] */
+  double* scal;                 /* [m][n_scal] */
+  int64_t* ints;                /* [m][FSMC_NINT] */
+  uint64_t seed;
+  unsigned long long* err_key;  /* [1]; (tick << 24) | chain of the first failure, ~0 = none */
+} fsmc_state;
+
+/* Per-sample observables of the CostLedger (lockstep.py:209-228). */
+typedef struct fsmc_outputs {
+  double* samples;              /* [n][m][dim] or NULL */
+  int32_t* loop_counts;         /* [L][n][m]: executions of each loop state per sample */
+  int32_t* sample_ticks;        /* [n][m] tick that finished each sample, or NULL */
+} fsmc_outputs;
+
+/* indices into fsmc_state.ints (per chain) */
+enum {
+  FSMC_I_COUNTER = 0, FSMC_I_STREAM = 1, FSMC_I_STATE = 2, FSMC_I_TICK = 3, FSMC_I_COUNT = 4,
+  FSMC_I_ERR_KIND = 5, FSMC_I_ERR_LABEL = 6, FSMC_I_ERR_TICK = 7, FSMC_I_ERR_ITER = 8,
+  FSMC_I_SHARED = 9, FSMC_I_BLOCKS = 10 /* 6 slots */, FSMC_I_PEND = 16 /* 3 slots */,
+  FSMC_I_FAMILY = 19 /* family-private slots 19..31 */
+};
+/* error kinds in FSMC_I_ERR_KIND */
+enum { FSMC_E_NONE = 0, FSMC_E_BLOCK = 1, FSMC_E_ZERO_START = 2, FSMC_E_GRAD = 3, FSMC_E_INIT = 4 };
+
+int32_t fsmc_abi_version(void);
+const char* fsmc_last_error(void);
+
+/* Slots a chain of this kernel needs (vectors of `dim` doubles, scalars). */
+fsmc_status fsmc_state_layout(const fsmc_kernel* k, int64_t dim, int32_t* n_vec,
+                              int32_t* n_scal, int32_t* n_loop_states, int32_t* n_states);
+
+/* Replaces prng.py:58-153 for bulk draws: out[i] = draw(seed, stream, counter+i).
+ * kind 0: raw 64-bit words (uint64 out), 1: uniform, 2: standard normal. */
+fsmc_status fsmc_prng_fill(uint64_t seed, uint64_t stream, uint64_t counter, int64_t count,
+                           int32_t kind, void* out, void* stream_);
+
+/* Replaces init_batch (lockstep.py:175-206): streams split(key(seed, parent_stream), .)
+ * for chains chain_offset .. chain_offset+m-1, start x0 (+ jitter draws), and the
+ * kernel's initial evaluation.  Failures land in the per-chain error slots and
+ * err_key (tick 0). */
+fsmc_status fsmc_init(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                      uint64_t parent_stream, int64_t chain_offset, const double* x0,
+                      double init_jitter, void* stream_);
+
+/* Replaces run_fsm_batched's tick loop (lockstep.py:308-406).  Each chain
+ * advances its own machine with no barrier.  mode 0: run each chain until it
+ * holds n samples (finishing the tick) or reaches tick_limit; mode 1: run
+ * each chain until tick_limit (the reference's surplus ticks).  `order` (host,
+ * K entries) is the bundled executor order.  lanes = lanes per chain (0: auto). */
+fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                     int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                     const fsmc_outputs* out, int32_t lanes, void* stream_);
+
+/* Replaces run_standard_batched (lockstep.py:238-305): the lock-step
+ * (vmap-style) baseline built from the same device blocks.  Every inner-loop
+ * iteration ends at a grid-wide barrier, so a sample costs max over chains of
+ * its loop count.  Chains beyond one co-resident wave run in successive
+ * waves, each with its own barriers. */
+fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                              int64_t n, const fsmc_outputs* out, int32_t lanes, void* stream_);
+
+/* Batched plugin evaluation: lp[j] = log p(X[j]), grad[j] (if non-NULL) for
+ * rows X[m][dim] (TargetModel.log_density / log_density_and_grad). */
+fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, double* lp,
+                             double* grad, void* stream_);
+
+/* Cross-chain diagnostic partials for effective_sample_size / R-hat
+ * (analysis.py:336-418).  samples [n][m][dim]; uses rows burn..n-1.
+ *   chain_mean [m][dim] (computed when lag0 == 0), acov [32][dim] = sum over chains of
+ *   the lag-(lag0+t) autocovariance (one tile of 32 lags per call;
+ *   divided by the row count, analysis.py:344-347). */
+fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int64_t dim,
+                               int64_t burn, int64_t lag0, int64_t n_lags, double* chain_mean,
+                               double* acov, void* stream_);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

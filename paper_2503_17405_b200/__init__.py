@@ -1,0 +1,23 @@
+"""B200-native multi-chain FSM MCMC engine (arXiv 2503.17405).
+
+Drop-in for the reference package ``fsm_mcmc``'s multi-chain sampling path:
+the same kernel builders, batch drivers, executors and plugin names, backed
+by hand-written sm_100a CUDA kernels (``libfsmc.so``, C ABI in
+``include/fsmc.h``).  There is no CPU fallback.
+"""
+
+from .fsm import (BlockFailure, FsmDefinition, FsmError, SharedComputation, StepOutcome,
+                  amortized_step, bundled_step, compose_nested, compose_sequential,
+                  compose_single_loop, step)
+from .kernels import KERNEL_BUILDERS, KernelBundle, KernelError, drmh_kernel, elliptical_kernel, \
+    nuts_kernel, slice_kernel
+from .lockstep import (ChainBatch, CostLedger, CostParams, KernelRunError, TickBudgetExceeded,
+                       collect_samples, init_batch, run_fsm_batched, run_standard_batched)
+from .prng import RngKey, key, normal, normal_vec, split, uniform, uniform_block
+from .targets import (GaussianPriorDecomposition, TargetError, TargetModel, conjugate_target,
+                      correlated_mog_target, equicorrelated_covariance,
+                      equicorrelated_gaussian_target, funnel_target, gaussian_target,
+                      gp_classification_target, standard_normal_target)
+from .analysis import EssSummary, effective_sample_size, rhat
+
+__version__ = "0.1.0"

@@ -1,0 +1,194 @@
+"""Cross-chain diagnostics on the device (drop-in for ``fsm_mcmc.analysis``'s ESS).
+
+``effective_sample_size`` follows ``analysis.py:336-418``: per-chain
+autocovariances, a chain-mean based var+, Geyer's initial positive pairs with
+the monotone fix, ESS = min(m n / tau, m n), pooled = min over dimensions.
+The partial sums (per-chain means, summed lag-t autocovariances) come from
+``fsmc_diag_partials`` in tiles of 32 lags, fetched only as far as Geyer's
+truncation needs.  The same partials are what the multi-GPU path all-reduces
+(``distributed.py``), so 1 GPU is the world-size-1 case of one code path.
+
+``rhat`` is Gelman-Rubin's potential scale reduction sqrt(var+ / W) from the
+same moments (new: the reference has none).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import warnings
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _lib
+
+__all__ = ["EssSummary", "effective_sample_size", "rhat", "DiagMoments", "diag_moments",
+           "ess_from_moments", "rhat_from_moments", "LAG_TILE"]
+
+LAG_TILE = 32
+
+
+@dataclass(frozen=True)
+class EssSummary:
+    per_dimension: tuple
+    pooled: float           # min across dimensions
+    per_cost: float | None
+    per_second: float | None
+    flagged: bool           # capped/floored somewhere
+
+
+@dataclass
+class DiagMoments:
+    """Everything ESS / R-hat need, summed over the chains it covers.
+
+    n: rows per chain; m: chains; sum_mean [d]; var_means [d] (ddof=1 across
+    chains); max_chain_var [d]; acov_tile(k) -> [32, d] sums over chains of the
+    lag 32k..32k+31 autocovariances (each / n, analysis.py:344-347).
+    """
+
+    n: int
+    m: int
+    d: int
+    var_means: np.ndarray
+    max_chain_var: np.ndarray
+    acov_tile: Callable[[int], np.ndarray]
+
+
+def _as_device(chains) -> torch.Tensor:
+    if isinstance(chains, torch.Tensor):
+        t = chains.to(device="cuda", dtype=torch.float64)
+    else:
+        t = torch.as_tensor(np.asarray(chains, dtype=np.float64), device="cuda")
+    if t.dim() == 2:
+        t = t[:, :, None]
+    if t.dim() != 3:
+        raise ValueError(f"expected an (n, m, d) array, got shape {tuple(t.shape)}")
+    return t.contiguous()
+
+
+def diag_moments(chains, burn: int = 0) -> DiagMoments:
+    """Per-device partial moments of samples [n, m, d] (rows burn..n-1)."""
+    S = _as_device(chains)
+    n_all, m, d = S.shape
+    n = n_all - burn
+    lib = _lib.lib()
+    mean = torch.empty((m, d), dtype=torch.float64, device="cuda")
+    tile = torch.empty((LAG_TILE, d), dtype=torch.float64, device="cuda")
+    _lib.check(lib.fsmc_diag_partials(S.data_ptr(), n_all, m, d, burn, 0, LAG_TILE,
+                                      mean.data_ptr(), tile.data_ptr(), _lib.stream_ptr()),
+               "fsmc_diag_partials")
+    first = tile.cpu().numpy()
+    var_means = mean.var(dim=0, unbiased=True).cpu().numpy() if m > 1 else np.zeros(d)
+    chain_var = S[burn:].var(dim=0, unbiased=False).amax(dim=0).cpu().numpy()
+
+    def acov_tile(k: int) -> np.ndarray:
+        if k == 0:
+            return first
+        _lib.check(lib.fsmc_diag_partials(S.data_ptr(), n_all, m, d, burn, k * LAG_TILE,
+                                          LAG_TILE, mean.data_ptr(), tile.data_ptr(),
+                                          _lib.stream_ptr()), "fsmc_diag_partials")
+        return tile.cpu().numpy()
+
+    return DiagMoments(n=n, m=m, d=d, var_means=var_means, max_chain_var=chain_var,
+                       acov_tile=acov_tile)
+
+
+class _Acov:
+    """Lazily tiled mean (over chains) autocovariance of one dimension set."""
+
+    def __init__(self, mom: DiagMoments):
+        self.mom = mom
+        self.tiles: list[np.ndarray] = []
+
+    def __call__(self, t: int, k: int) -> float:
+        tile = t // LAG_TILE
+        while len(self.tiles) <= tile:
+            self.tiles.append(self.mom.acov_tile(len(self.tiles)) / self.mom.m)
+        return float(self.tiles[tile][t % LAG_TILE, k])
+
+
+def _ess_dim(ac: _Acov, mom: DiagMoments, k: int) -> tuple[float, bool]:
+    """analysis.py:336-386 for dimension k."""
+    m, n = mom.m, mom.n
+    total = m * n
+    if mom.max_chain_var[k] <= 1e-8:   # np.allclose(var, 0)
+        warnings.warn("constant chain: ESS floored to 1", stacklevel=3)
+        return 1.0, True
+    mean_var = ac(0, k) * n / (n - 1.0)
+    var_plus = mean_var * (n - 1.0) / n
+    if m > 1:
+        var_plus += float(mom.var_means[k])
+    rho = {0: 1.0}
+    rho_even = 1.0
+    rho_odd = 1.0 - (mean_var - ac(1, k)) / var_plus
+    rho[1] = rho_odd
+    anticorrelated = (rho_even + rho_odd) < 0.0
+    t = 1
+    while t < n - 2 and (rho_even + rho_odd) >= 0.0:
+        rho_even = 1.0 - (mean_var - ac(t + 1, k)) / var_plus
+        rho_odd = 1.0 - (mean_var - ac(t + 2, k)) / var_plus
+        rho[t + 1] = rho_even
+        if (rho_even + rho_odd) >= 0.0:
+            rho[t + 2] = rho_odd
+        t += 2
+    max_t = t
+    t = 1
+    while t <= max_t - 2:   # initial monotone sequence
+        if rho.get(t + 1, 0.0) + rho.get(t + 2, 0.0) > rho.get(t - 1, 0.0) + rho.get(t, 0.0):
+            rho[t + 1] = (rho.get(t - 1, 0.0) + rho.get(t, 0.0)) / 2.0
+            rho[t + 2] = rho[t + 1]
+        t += 2
+    tau = -1.0 + 2.0 * sum(rho.get(i, 0.0) for i in range(max_t)) + \
+        (rho.get(max_t + 1, 0.0) if max_t + 1 < n else 0.0)
+    flagged = False
+    if tau <= 0 or not math.isfinite(tau):
+        tau = 1.0 / total
+        flagged = True
+    ess = total / tau
+    if anticorrelated:
+        warnings.warn("anticorrelated chain: ESS capped at the sample count", stacklevel=3)
+        flagged = True
+    return float(min(ess, float(total))), flagged
+
+
+def ess_from_moments(mom: DiagMoments, model_cost=None, walltime=None) -> EssSummary:
+    ac = _Acov(mom)
+    per_dim, flagged = [], False
+    for k in range(mom.d):
+        e, f = _ess_dim(ac, mom, k)
+        per_dim.append(e)
+        flagged = flagged or f
+    pooled = min(per_dim)
+    return EssSummary(per_dimension=tuple(per_dim), pooled=pooled,
+                      per_cost=pooled / model_cost if model_cost else None,
+                      per_second=pooled / walltime if walltime else None, flagged=flagged)
+
+
+def effective_sample_size(chains, model_cost: float | None = None,
+                          walltime: float | None = None, burn: int = 0) -> EssSummary:
+    """Autocorrelation-adjusted sample count of an (n, m, d) array (analysis.py:389-418)."""
+    shape = tuple(chains.shape)
+    n = shape[0] - burn
+    if len(shape) not in (2, 3):
+        raise ValueError(f"expected an (n, m, d) array, got shape {shape}")
+    if n < 10:
+        raise ValueError(f"need at least 10 samples per chain, got {n}")
+    return ess_from_moments(diag_moments(chains, burn), model_cost, walltime)
+
+
+def rhat_from_moments(mom: DiagMoments) -> np.ndarray:
+    """Potential scale reduction sqrt(var+ / W) per dimension."""
+    tile0 = mom.acov_tile(0)[0] / mom.m
+    n = mom.n
+    W = tile0 * n / (n - 1.0)
+    var_plus = W * (n - 1.0) / n + (mom.var_means if mom.m > 1 else 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return np.sqrt(var_plus / W)
+
+
+def rhat(chains, burn: int = 0) -> np.ndarray:
+    """Gelman-Rubin R-hat per dimension of an (n, m, d) array."""
+    return rhat_from_moments(diag_moments(chains, burn))

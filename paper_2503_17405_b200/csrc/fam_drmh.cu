@@ -1,0 +1,13 @@
+// fam_drmh.cu -- Drmh kernels for the compiled (lanes, elements) pairs.
+#include "kernels.cuh"
+
+namespace fsmc {
+cudaError_t dispatch_drmh(int op, int g, int e, Params& p, const LaunchCtx& lc, cudaStream_t s,
+                           uint64_t ps, long long off, const double* x0, double jit) {
+#define X(GG, EE) \
+  if (g == GG && e == EE) return launch_op<Drmh, GG, EE>(op, p, lc, s, ps, off, x0, jit);
+  FSMC_DRMH_CONFIGS(X)
+#undef X
+  return cudaErrorInvalidConfiguration;
+}
+}  // namespace fsmc

@@ -1,0 +1,361 @@
+// fsmc.cu -- kernels and C-ABI entry points of libfsmc.so (see include/fsmc.h).
+//
+//   fsm_init_kernel      init_batch                     lockstep.py:175-206
+//   fsm_run_kernel       run_fsm_batched tick loop      lockstep.py:308-406
+//   lockstep_kernel      run_standard_batched           lockstep.py:238-305
+//   prng_fill_kernel     prng.uniform/normal/_bits      prng.py:58-153
+//   target_eval_kernel   TargetModel.log_density(_and_grad)
+//
+// Chains are independent (prng.py:84-94), so fsm_run_kernel gives every lane
+// group a chain from a dynamic queue and runs it to completion with its
+// state in registers: no barrier, no per-tick HBM round trip.  Only the
+// lock-step baseline synchronises (a grid barrier per inner iteration).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "kernels.cuh"
+
+using namespace fsmc;
+
+namespace {
+thread_local std::string g_last_error;
+fsmc_status fail(fsmc_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+#define CUDA_TRY(expr)                                                               \
+  do {                                                                               \
+    cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(FSMC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+// per-device scratch: chain queue, barrier words
+struct Scratch {
+  unsigned* words = nullptr;  // [0] queue, [1] bar_count, [2] bar_gen, [3..4] active flags
+};
+Scratch& scratch() {
+  static Scratch s;
+  if (!s.words) cudaMalloc(&s.words, 64 * sizeof(unsigned));
+  return s;
+}
+}  // namespace
+
+// --------------------------------------------------------------- utilities
+__global__ void prng_fill_kernel(uint64_t seed, uint64_t stream, uint64_t counter, long long count,
+                                 int kind, void* out) {
+  uint64_t hsc = hash_seed_stream(seed, stream);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    uint64_t ctr = counter + (uint64_t)i;
+    if (kind == 0)
+      ((uint64_t*)out)[i] = bits(hsc, ctr);
+    else if (kind == 1)
+      ((double*)out)[i] = uniform(hsc, ctr);
+    else
+      ((double*)out)[i] = normal(hsc, ctr);
+  }
+}
+
+template <int G, int E>
+__global__ void __launch_bounds__(kThreads) target_eval_kernel(fsmc_target t, const double* X,
+                                                               long long m, double* lp, double* grad) {
+  extern __shared__ double smem[];
+  Grp<G> grp;
+  double* sm = smem + (size_t)(threadIdx.x / G) * t.dim;
+  const int d = t.dim;
+  const long long groups = (long long)gridDim.x * (kThreads / G);
+  for (long long j = (long long)blockIdx.x * (kThreads / G) + threadIdx.x / G; j < m; j += groups) {
+    double x[E], g[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      int i = grp.idx(e);
+      x[e] = i < d ? X[(size_t)j * d + i] : 0.0;
+    }
+    double v = grad ? target_eval<G, E, true>(t, x, g, sm, grp) : target_lp<G, E>(t, x, sm, grp);
+    if (grp.lane == 0) lp[j] = v;
+    if (grad) {
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        int i = grp.idx(e);
+        if (i < d) grad[(size_t)j * d + i] = g[e];
+      }
+    }
+  }
+}
+
+// diagnostics: per-chain means and cross-chain summed autocovariances
+// (analysis.py:344-352).  One block per (dim, lag tile).
+__global__ void diag_mean_kernel(const double* S, long long n, long long m, long long d, long long burn,
+                                 double* mean) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= m * d) return;
+  long long j = idx / d, k = idx % d;
+  double s = 0.0;
+  for (long long i = burn; i < n; i++) s += S[((size_t)i * m + j) * d + k];
+  mean[idx] = s / (double)(n - burn);
+}
+
+constexpr int kLagTile = 32;
+// thread per (chain, dim): lags lag0 .. lag0+kLagTile-1 of the centred series,
+// accumulated into acov[t][k] (sum over chains).  Warps read consecutive
+// (chain, dim) addresses of one sample row, so the row loads coalesce.
+__global__ void diag_acov_kernel(const double* S, long long n, long long m, long long d, long long burn,
+                                 long long lag0, const double* mean, double* acov) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= m * d) return;
+  const long long k = idx % d;
+  const long long N = n - burn;
+  const double mu = mean[idx];
+  double acc[kLagTile];
+#pragma unroll
+  for (int t = 0; t < kLagTile; t++) acc[t] = 0.0;
+  const size_t stride = (size_t)m * d;
+  const double* col = S + (size_t)burn * stride + idx;
+  for (long long i = 0; i + lag0 < N; i++) {
+    double ci = col[(size_t)i * stride] - mu;
+#pragma unroll
+    for (int t = 0; t < kLagTile; t++) {
+      long long ii = i + lag0 + t;
+      if (ii < N) acc[t] += ci * (col[(size_t)ii * stride] - mu);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kLagTile; t++)
+    if (lag0 + t < N) atomicAdd(&acov[t * d + k], acc[t] / (double)N);
+}
+
+// ================================================================ dispatch
+namespace fsmc {
+cudaError_t dispatch_drmh(int, int, int, Params&, const LaunchCtx&, cudaStream_t, uint64_t, long long,
+                          const double*, double);
+cudaError_t dispatch_ess(int, int, int, Params&, const LaunchCtx&, cudaStream_t, uint64_t, long long,
+                         const double*, double);
+cudaError_t dispatch_nuts(int, int, int, Params&, const LaunchCtx&, cudaStream_t, uint64_t, long long,
+                          const double*, double);
+}  // namespace fsmc
+
+namespace {
+
+struct GE {
+  int g, e;
+};
+
+// smallest compiled E for the requested lanes (auto: thread-per-chain for
+// small d, a warp per chain beyond)
+bool pick_config(int family, int dim, int lanes, GE& out) {
+  static const GE drmh[] = {
+#define X(GG, EE) {GG, EE},
+      FSMC_DRMH_CONFIGS(X)};
+  static const GE ess[] = {FSMC_ESS_CONFIGS(X)};
+  static const GE nuts[] = {FSMC_NUTS_CONFIGS(X)};
+#undef X
+  const GE* list = family == FSMC_DRMH ? drmh : family == FSMC_ESS ? ess : nuts;
+  int cnt = family == FSMC_DRMH ? (int)(sizeof(drmh) / sizeof(GE))
+            : family == FSMC_ESS ? (int)(sizeof(ess) / sizeof(GE))
+                                 : (int)(sizeof(nuts) / sizeof(GE));
+  if (lanes <= 0) {
+    if (family == FSMC_DRMH && dim <= 16) lanes = 1;
+    else if (dim <= 4) lanes = 1;
+    else if (family == FSMC_NUTS && dim <= 16) lanes = 4;
+    else lanes = 32;
+  }
+  const GE* best = nullptr;
+  for (int i = 0; i < cnt; i++) {
+    const GE& c = list[i];
+    if (c.g != lanes || c.g * c.e < dim) continue;
+    if (!best || c.e < best->e) best = &c;
+  }
+  if (!best && lanes == 1) return pick_config(family, dim, family == FSMC_NUTS && dim <= 16 ? 4 : 32, out);
+  if (!best) return false;
+  out = *best;
+  return true;
+}
+
+LaunchCtx launch_ctx() {
+  LaunchCtx lc;
+  lc.num_sms = num_sms();
+  lc.words = scratch().words;
+  return lc;
+}
+
+cudaError_t dispatch_family(int op, const GE& ge, Params& p, cudaStream_t s, uint64_t ps = 0,
+                            long long off = 0, const double* x0 = nullptr, double jit = 0.0) {
+  LaunchCtx lc = launch_ctx();
+  switch (p.k.family) {
+    case FSMC_DRMH: return dispatch_drmh(op, ge.g, ge.e, p, lc, s, ps, off, x0, jit);
+    case FSMC_ESS: return dispatch_ess(op, ge.g, ge.e, p, lc, s, ps, off, x0, jit);
+    default: return dispatch_nuts(op, ge.g, ge.e, p, lc, s, ps, off, x0, jit);
+  }
+}
+
+fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_state* st) {
+  if (!k || !t || !st) return fail(FSMC_ERR_ARG, "null argument");
+  if (k->family < FSMC_DRMH || k->family > FSMC_NUTS) return fail(FSMC_ERR_ARG, "unknown kernel family");
+  if (t->dim < 1) return fail(FSMC_ERR_ARG, "dim must be >= 1");
+  if (st->dim != t->dim) return fail(FSMC_ERR_ARG, "state dim does not match target dim");
+  if (st->m < 1 || st->m >= (1LL << 24)) return fail(FSMC_ERR_ARG, "m must be in [1, 2^24) per state block");
+  if (k->family == FSMC_DRMH && (k->max_tries < 1 || !(k->proposal_scale > 0)))
+    return fail(FSMC_ERR_ARG, "invalid drmh parameters");
+  if (k->family == FSMC_NUTS && (k->max_depth < 1 || k->max_depth > 40 || !(k->step_size > 0)))
+    return fail(FSMC_ERR_ARG, "invalid nuts parameters");
+  if (k->family == FSMC_ESS && t->prior_kind == FSMC_PRIOR_NONE)
+    return fail(FSMC_ERR_ARG, "elliptical slice sampling needs a Gaussian-prior split");
+  if (t->kind == FSMC_T_MOG && (t->n_modes < 1 || t->n_modes > FSMC_MAX_MODES))
+    return fail(FSMC_ERR_ARG, "n_modes out of range");
+  return FSMC_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int32_t fsmc_abi_version(void) { return FSMC_ABI_VERSION; }
+const char* fsmc_last_error(void) { return g_last_error.c_str(); }
+
+fsmc_status fsmc_state_layout(const fsmc_kernel* k, int64_t dim, int32_t* n_vec, int32_t* n_scal,
+                              int32_t* n_loop, int32_t* n_states) {
+  if (!k) return fail(FSMC_ERR_ARG, "null kernel");
+  switch (k->family) {
+    case FSMC_DRMH: *n_vec = 2; *n_scal = 3; *n_loop = 1; *n_states = 3; break;
+    case FSMC_ESS: *n_vec = 3; *n_scal = 6; *n_loop = 1; *n_states = 3; break;
+    case FSMC_NUTS:
+      *n_vec = 12 + 2 * k->max_depth; *n_scal = 3; *n_loop = 3; *n_states = 5;
+      break;
+    default: return fail(FSMC_ERR_ARG, "unknown kernel family");
+  }
+  (void)dim;
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_prng_fill(uint64_t seed, uint64_t stream, uint64_t counter, int64_t count, int32_t kind,
+                           void* out, void* stream_) {
+  if (count < 0 || kind < 0 || kind > 2 || (!out && count)) return fail(FSMC_ERR_ARG, "bad prng_fill args");
+  if (!count) return FSMC_OK;
+  int blocks = (int)std::min<long long>((count + 255) / 256, 148LL * 16);
+  prng_fill_kernel<<<blocks, 256, 0, (cudaStream_t)stream_>>>(seed, stream, counter, count, kind, out);
+  CUDA_TRY(cudaGetLastError());
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_init(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, uint64_t parent_stream,
+                      int64_t chain_offset, const double* x0, double init_jitter, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  GE ge;
+  if (!pick_config(k->family, t->dim, 0, ge)) return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  cudaStream_t cs = (cudaStream_t)stream_;
+  CUDA_TRY(cudaMemsetAsync(st->err_key, 0xff, sizeof(unsigned long long), cs));
+  CUDA_TRY(dispatch_family(0, ge, p, cs, parent_stream, chain_offset, x0, init_jitter));
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n, int32_t variant,
+                     const int32_t* order, int64_t tick_limit, int32_t mode, const fsmc_outputs* out,
+                     int32_t lanes, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (n < 0) return fail(FSMC_ERR_ARG, "n must be >= 0");
+  if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
+  GE ge;
+  if (!pick_config(k->family, t->dim, lanes, ge))
+    return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  if (out) p.out = *out;
+  p.n = n;
+  p.tick_limit = tick_limit;
+  p.variant = variant;
+  p.mode = mode;
+  int K = k->family == FSMC_NUTS ? 5 : 3;
+  for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
+  cudaStream_t cs = (cudaStream_t)stream_;
+  p.next_chain = scratch().words;
+  CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
+  CUDA_TRY(dispatch_family(1, ge, p, cs));
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                              const fsmc_outputs* out, int32_t lanes, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  GE ge;
+  if (!pick_config(k->family, t->dim, lanes, ge))
+    return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  if (out) p.out = *out;
+  p.n = n;
+  cudaStream_t cs = (cudaStream_t)stream_;
+  unsigned* w = scratch().words;
+  p.bar_count = w + 1;
+  p.bar_gen = w + 2;
+  p.active_flags = w + 3;
+  CUDA_TRY(cudaMemsetAsync(w + 1, 0, 4 * sizeof(unsigned), cs));
+  CUDA_TRY(dispatch_family(2, ge, p, cs));
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, double* lp, double* grad,
+                             void* stream_) {
+  if (!t || !X || !lp || m < 0) return fail(FSMC_ERR_ARG, "bad target_eval args");
+  if (!m) return FSMC_OK;
+  GE ge;
+  if (!pick_config(FSMC_ESS, t->dim, 0, ge)) return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+  cudaStream_t cs = (cudaStream_t)stream_;
+  size_t sm = (size_t)(kThreads / ge.g) * t->dim * sizeof(double);
+  long long groups = (m + kThreads / ge.g - 1) / (kThreads / ge.g);
+  int blocks = (int)std::min<long long>(groups, 148LL * 8);
+#define X(GG, EE)                                                                           \
+  if (ge.g == GG && ge.e == EE) {                                                           \
+    target_eval_kernel<GG, EE><<<blocks, kThreads, sm, cs>>>(*t, X, m, lp, grad);           \
+    CUDA_TRY(cudaGetLastError());                                                         \
+    return FSMC_OK;                                                                       \
+  }
+  FSMC_ESS_CONFIGS(X)
+#undef X
+  return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+}
+
+fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int64_t dim, int64_t burn,
+                               int64_t lag0, int64_t n_lags, double* chain_mean, double* acov,
+                               void* stream_) {
+  if (!samples || n - burn < 2 || m < 1 || dim < 1 || !chain_mean) return fail(FSMC_ERR_ARG, "bad diag args");
+  cudaStream_t cs = (cudaStream_t)stream_;
+  if (lag0 == 0) {
+    long long tot = m * dim;
+    diag_mean_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, cs>>>(samples, n, m, dim, burn, chain_mean);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (n_lags > 0 && acov) {
+    if (n_lags != kLagTile) return fail(FSMC_ERR_ARG, "n_lags must be 32 (one lag tile per call)");
+    CUDA_TRY(cudaMemsetAsync(acov, 0, sizeof(double) * kLagTile * dim, cs));
+    long long tot = m * dim;
+    diag_acov_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, cs>>>(samples, n, m, dim, burn, lag0,
+                                                                    chain_mean, acov);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return FSMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,251 @@
+// kernels.cuh -- the three per-family kernels and their launchers.
+//
+//   fsm_init_kernel   init_batch                     lockstep.py:175-206
+//   fsm_run_kernel    run_fsm_batched tick loop      lockstep.py:308-406
+//   lockstep_kernel   run_standard_batched           lockstep.py:238-305
+//
+// Included by one translation unit per family (fam_*.cu) so the families
+// compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "configs.h"
+#include "fsm_device.cuh"
+
+namespace fsmc {
+
+constexpr int kThreads = 128;
+
+struct LaunchCtx {
+  int num_sms;
+  unsigned* words;  // [0] chain queue, [1] barrier count, [2] barrier generation, [3..4] flags
+};
+
+// ---------------------------------------------------------------- init
+template <template <int, int> class F, int G, int E>
+__global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t parent_stream,
+                                                            long long chain_offset, const double* x0,
+                                                            double jitter) {
+  extern __shared__ double smem[];
+  Grp<G> grp;
+  const int gib = threadIdx.x / G;
+  double* sm = smem + (size_t)gib * p.t.dim;
+  const long long groups = (long long)gridDim.x * (kThreads / G);
+  const int d = p.t.dim;
+  for (long long j = (long long)blockIdx.x * (kThreads / G) + gib; j < p.st.m; j += groups) {
+    Core c;
+    memset(&c, 0, sizeof(c));
+    uint64_t stream = split_stream(parent_stream, (uint64_t)(chain_offset + j));  // prng.py:84-94
+    c.hsc = hash_seed_stream(p.st.seed, stream);
+    c.state = 1;
+    F<G, E> f;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      int i = grp.idx(e);
+      f.x[e] = (i < d && x0) ? x0[i] : 0.0;
+    }
+    if (jitter > 0.0) {  // lockstep.py:195-198: N(0, jitter^2 I) offset drawn first
+      double eps[E];
+      normal_vec<G, E>(c, d, eps, grp);
+#pragma unroll
+      for (int e = 0; e < E; e++) f.x[e] = f.x[e] + jitter * eps[e];
+    }
+    bool ok = true;
+    if constexpr (F<G, E>::K == 5) {
+      f.init_state();
+      f.ck = nullptr;
+    } else {
+      f.init_pre();
+      double lp = target_eval<G, E, false>(p.t, f.ev(), f.evg(), sm, grp);
+      ok = f.init_post(c, lp);
+    }
+    f.store(p, j, grp);
+    if (grp.lane == 0) {
+      core_store(c, p, j);
+      p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_STREAM] = (int64_t)stream;
+      if (!ok) report_error(c, p, j);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- run
+// Every lane group pulls chains from a queue and runs each to completion
+// with its state in registers.  No barrier anywhere: chains in different
+// states simply execute different blocks.
+template <template <int, int> class F, int G, int E>
+__global__ void __launch_bounds__(kThreads) fsm_run_kernel(Params p) {
+  extern __shared__ double smem[];
+  Grp<G> grp;
+  double* sm = smem + (size_t)(threadIdx.x / G) * p.t.dim;
+  while (true) {
+    long long j = 0;
+    if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
+    j = grp.bcast_ll(j, 0);
+    if (j >= p.st.m) break;
+    Core c;
+    core_load(c, p, j);
+    if (c.err_kind != FSMC_E_NONE) continue;
+    F<G, E> f;
+    f.load(p, j, grp);
+    bool ok = true;
+    const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
+#pragma unroll 1
+    while (c.count < n_stop && c.tick < p.tick_limit)
+      if (!tick<F<G, E>, G, E>(p, c, f, sm, j, grp)) { ok = false; break; }
+    f.store(p, j, grp);
+    if (grp.lane == 0) {
+      core_store(c, p, j);
+      if (!ok) report_error(c, p, j);
+    }
+  }
+}
+
+// ------------------------------------------------------------ lock-step
+// Grid-wide "any" + barrier.  Every thread of the (cooperatively launched,
+// hence co-resident) grid calls it the same number of times.
+__device__ __forceinline__ bool grid_any(const Params& p, bool pred, unsigned& phase) {
+  int blk = __syncthreads_or(pred ? 1 : 0);
+  if (threadIdx.x == 0) {
+    if (blk) atomicOr(&p.active_flags[phase & 1], 1u);
+    __threadfence();
+    unsigned gen = *p.bar_gen;
+    if (atomicAdd(p.bar_count, 1u) == gridDim.x - 1) {
+      *p.bar_count = 0;
+      p.active_flags[(phase + 1) & 1] = 0;
+      __threadfence();
+      atomicAdd((unsigned*)p.bar_gen, 1u);
+    } else {
+      while (*p.bar_gen == gen) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  bool any = ((volatile unsigned*)p.active_flags)[phase & 1] != 0;
+  phase++;
+  return any;
+}
+
+// vmap semantics of each kernel's monolithic sampler (drmh.py:163-169,
+// elliptical.py:122-132, nuts.py:237-248): every while-loop test is a
+// barrier across all chains of the wave, so a sample costs max over chains of
+// its loop count.  Written as a uniform program counter so the state body
+// (and its log-density evaluation) is instantiated once.
+template <template <int, int> class F, int G, int E>
+__global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
+  using FF = F<G, E>;
+  extern __shared__ double smem[];
+  Grp<G> grp;
+  double* sm = smem + (size_t)(threadIdx.x / G) * p.t.dim;
+  const long long j = p.wave_lo + (long long)blockIdx.x * (kThreads / G) + threadIdx.x / G;
+  bool live = j < p.wave_hi;
+  Core c;
+  FF f;
+  if (live) {
+    core_load(c, p, j);
+    f.load(p, j, grp);
+    live = c.err_kind == FSMC_E_NONE;
+  }
+  enum { PC_INIT, PC_OUTER, PC_INNER, PC_END };
+  unsigned phase = 0;
+#pragma unroll 1
+  for (long long i = 0; i < p.n; i++) {
+    if (live) { c.count = i; c.tick = i; c.pend[0] = c.pend[1] = c.pend[2] = 0; }
+    int pc = PC_INIT;
+    bool outer = false;
+#pragma unroll 1
+    while (true) {
+      int s = 0;
+      if (pc == PC_INIT) {
+        s = 1;
+        pc = PC_OUTER;
+      } else if constexpr (FF::K == 5) {
+        if (pc == PC_OUTER) {  // while _outer_continue(z)
+          bool co = live && f.outer_continue(p);
+          if (!grid_any(p, co, phase)) { s = 5; pc = PC_END; }
+          else { outer = co; s = co ? 2 : 0; pc = PC_INNER; }
+        } else {  // while _inner_continue(z)
+          bool ci = outer && live && f.inner_continue();
+          if (grid_any(p, ci, phase)) s = ci ? 3 : 0;
+          else { s = (outer && live) ? 4 : 0; pc = PC_OUTER; }
+        }
+      } else {  // while _continue(z) / _below_threshold(z)
+        bool co = live && f.loop_continue(p);
+        if (grid_any(p, co, phase)) s = co ? 2 : 0;
+        else { s = 3; pc = PC_END; }
+      }
+      if (live && s) {
+        bool did = false;
+        if (!run_state<FF, G, E>(p, c, f, s, did, sm, grp)) live = false;
+        count_block<FF>(c, s);
+        if (did) c.shared++;
+      }
+      if (pc == PC_END) break;
+    }
+    // per-sample loop counts were accumulated in pend by count_block
+    if (live) flush_sample<FF, G, E>(p, c, f, j, grp);
+  }
+  if (j < p.wave_hi) {
+    f.store(p, j, grp);
+    if (grp.lane == 0) {
+      core_store(c, p, j);
+      if (c.err_kind != FSMC_E_NONE) report_error(c, p, j);
+    }
+  }
+}
+
+// ------------------------------------------------------------- launchers
+template <template <int, int> class F, int G, int E>
+struct Launch {
+  static size_t smem(const Params& p) { return (size_t)(kThreads / G) * p.t.dim * sizeof(double); }
+  static cudaError_t init(const Params& p, uint64_t ps, long long off, const double* x0, double jit,
+                          cudaStream_t s) {
+    long long groups = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
+    int blocks = (int)std::min<long long>(groups, 1 << 20);
+    fsm_init_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p, ps, off, x0, jit);
+    return cudaGetLastError();
+  }
+  static cudaError_t run(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_run_kernel<F, G, E>,
+                                                                  kThreads, smem(p));
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
+    int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
+    fsm_run_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t lockstep(Params p, const LaunchCtx& lc, cudaStream_t s) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lockstep_kernel<F, G, E>,
+                                                                  kThreads, smem(p));
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    const long long per_block = kThreads / G;
+    const long long cap = (long long)occ * lc.num_sms * per_block;
+    for (long long lo = 0; lo < p.st.m; lo += cap) {
+      p.wave_lo = lo;
+      p.wave_hi = std::min<long long>(p.st.m, lo + cap);
+      int blocks = (int)((p.wave_hi - lo + per_block - 1) / per_block);
+      void* args[] = {&p};
+      e = cudaLaunchCooperativeKernel((const void*)lockstep_kernel<F, G, E>, dim3(blocks),
+                                      dim3(kThreads), args, smem(p), s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+};
+
+// op: 0 init, 1 run, 2 lock-step
+template <template <int, int> class F, int G, int E>
+cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, uint64_t ps,
+                      long long off, const double* x0, double jit) {
+  if (op == 0) return Launch<F, G, E>::init(p, ps, off, x0, jit, s);
+  if (op == 1) return Launch<F, G, E>::run(p, lc, s);
+  return Launch<F, G, E>::lockstep(p, lc, s);
+}
+
+}  // namespace fsmc

@@ -1,0 +1,469 @@
+"""Batched chain drivers (drop-in for ``fsm_mcmc.lockstep``).
+
+* :func:`init_batch` -> one ``fsmc_init`` launch: streams, starting points
+  and each kernel's initial evaluation for m chains (``lockstep.py:175-206``).
+* :func:`run_fsm_batched` -> ``fsmc_run``: every chain advances its own
+  state machine with no barrier until it holds n samples; per-chain tick
+  counters equal the reference's global ticks because the reference steps
+  every chain once per tick (``lockstep.py:359-406``).  The chunked global
+  stop rule and the surplus ticks the aggregate counters include are
+  reproduced exactly by a second, count-only launch.
+* :func:`run_standard_batched` -> ``fsmc_lockstep_run``: the lock-step
+  (vmap-style) baseline built from the same device blocks.
+
+Samples and ledgers come back as numpy arrays (``output="numpy"``, the
+reference's types) or stay in HBM as torch tensors (``output="torch"``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import Any, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .fsm import BlockFailure, ChainView, FsmDefinition, StepOutcome, default_bundled_order, \
+    validate_bundled_order
+from .prng import RngKey
+
+__all__ = ["ChainBatch", "CostParams", "CostLedger", "KernelRunError", "TickBudgetExceeded",
+           "init_batch", "run_standard_batched", "run_fsm_batched", "collect_samples",
+           "STEP_VARIANTS", "TICK_CHUNK"]
+
+STEP_VARIANTS = ("plain", "bundled", "amortized")
+TICK_CHUNK = 100
+_VARIANT_ID = {"plain": _lib.PLAIN, "bundled": _lib.BUNDLED, "amortized": _lib.AMORTIZED}
+_NO_LIMIT = 1 << 62
+
+
+class KernelRunError(RuntimeError):
+    """A kernel failed mid-run; records which chain and where (lockstep.py:50-57)."""
+
+    def __init__(self, chain: int, iteration: int, cause: Exception):
+        super().__init__(f"chain {chain}, sample index {iteration}: {cause}")
+        self.chain = chain
+        self.iteration = iteration
+        self.cause = cause
+
+
+class TickBudgetExceeded(RuntimeError):
+    """The FSM loop hit its tick cap; the partial ledger is attached (lockstep.py:60-68)."""
+
+    def __init__(self, budget: int, ledger: "CostLedger", sample_counts: list):
+        super().__init__(f"tick budget {budget} exhausted with per-chain sample counts "
+                         f"{sample_counts}")
+        self.ledger = ledger
+        self.sample_counts = sample_counts
+
+
+@dataclass(frozen=True)
+class CostParams:
+    """Abstract block costs c_1..c_K, dispatch factor alpha and shared-site
+    pricing (lockstep.py:71-155).  Host arithmetic over device counts."""
+
+    block_costs: tuple
+    alpha: float = 1.0
+    loop_states: tuple = ()
+    shared_cost: float = 0.0
+    shared_sites: tuple = ()
+
+    def __post_init__(self):
+        if len(self.block_costs) < 1:
+            raise ValueError("need at least one block cost")
+        if any(c < 0 for c in self.block_costs):
+            raise ValueError(f"block costs must be nonnegative: {self.block_costs}")
+        if self.shared_cost < 0:
+            raise ValueError("shared_cost must be nonnegative")
+        sites = tuple(self.shared_sites) or (0,) * len(self.block_costs)
+        if len(sites) != len(self.block_costs):
+            raise ValueError("shared_sites length must match block_costs")
+        object.__setattr__(self, "shared_sites", sites)
+        full = self.full_block_costs()
+        if sum(full) <= 0:
+            raise ValueError("total block cost must be positive")
+        lo = max(full) / sum(full)
+        if not lo - 1e-12 <= self.alpha <= 1.0 + 1e-12:
+            raise ValueError(f"alpha={self.alpha} outside admissible interval [{lo}, 1]")
+        K = len(self.block_costs)
+        if any(not 1 <= s <= K for s in self.loop_states):
+            raise ValueError(f"loop_states {self.loop_states} outside 1..{K}")
+
+    def full_block_costs(self) -> tuple:
+        return tuple(c + s * self.shared_cost for c, s in zip(self.block_costs, self.shared_sites))
+
+    def tick_cost(self, variant: str) -> float:
+        """Charge of one executor call over the batch (lockstep.py:119-131)."""
+        if variant in ("plain", "bundled"):
+            return self.alpha * sum(self.full_block_costs())
+        if variant == "amortized":
+            extra = self.shared_cost if sum(self.shared_sites) > 0 else 0.0
+            return self.alpha * sum(self.block_costs) + extra
+        raise ValueError(f"unknown step variant {variant!r}")
+
+    def shared_evals_per_tick(self, variant: str) -> int:
+        if sum(self.shared_sites) == 0:
+            return 0
+        return int(sum(self.shared_sites)) if variant in ("plain", "bundled") else 1
+
+    @staticmethod
+    def for_fsm(fsm: FsmDefinition, block_costs=None, alpha: float = 1.0,
+                shared_cost: float = 1.0) -> "CostParams":
+        K = fsm.n_states
+        costs = tuple(block_costs) if block_costs is not None else (1.0,) * K
+        sites = tuple(fsm.shared.sites.get(k, 0) for k in range(1, K + 1)) \
+            if fsm.shared is not None else (0,) * K
+        return CostParams(block_costs=costs, alpha=alpha, loop_states=tuple(sorted(fsm.loop_states)),
+                          shared_cost=shared_cost if fsm.shared is not None else 0.0,
+                          shared_sites=sites)
+
+
+@dataclass
+class CostLedger:
+    """Counts and model charges of one run (lockstep.py:209-228)."""
+
+    iter_counts: Any
+    loop_exec_counts: dict
+    tick_count: int
+    block_exec_counts: Any
+    charged_cost: float
+    walltime: float
+    regime: str
+    tick_cost: float = 0.0
+    shared_evals_per_tick: int = 0
+    native_shared_evals: int = 0
+    sample_ticks: Any = None
+    extras: dict = field(default_factory=dict)
+
+    def cost_per_sample(self) -> float:
+        return self.charged_cost / self.iter_counts.shape[0]
+
+
+# ------------------------------------------------------------------ batch
+class ChainBatch:
+    """m chains in structure-of-arrays device state (lockstep.py:158-172).
+
+    vec [m, n_vec, d] float64, scal [m, n_scal] float64, ints [m, 32] int64
+    (counter, stream, state, tick, count, error record, block counts,
+    family-private integers), err_key [1].
+    """
+
+    def __init__(self, bundle, target, m: int, seed: int, parent_stream: int = 0,
+                 chain_offset: int = 0):
+        lib = _lib.lib()
+        self.bundle, self.target, self.m, self.seed = bundle, target, int(m), int(seed)
+        self.parent_stream, self.chain_offset = int(parent_stream), int(chain_offset)
+        self.kernel = bundle.struct()
+        nv, ns, nl, nk = (ctypes.c_int32() for _ in range(4))
+        _lib.check(lib.fsmc_state_layout(ctypes.byref(self.kernel), target.dim, ctypes.byref(nv),
+                                         ctypes.byref(ns), ctypes.byref(nl), ctypes.byref(nk)),
+                   "fsmc_state_layout")
+        self.n_vec, self.n_scal, self.n_loop, self.n_states = nv.value, ns.value, nl.value, nk.value
+        d = target.dim
+        self.vec = torch.zeros((self.m, self.n_vec, d), dtype=torch.float64, device="cuda")
+        self.scal = torch.zeros((self.m, self.n_scal), dtype=torch.float64, device="cuda")
+        self.ints = torch.zeros((self.m, _lib.FSMC_NINT), dtype=torch.int64, device="cuda")
+        self.err_key = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        self.active_mask = [True] * self.m
+
+    def struct(self, lo: int = 0, hi: int | None = None) -> _lib.State:
+        hi = self.m if hi is None else hi
+        s = _lib.State()
+        s.m = hi - lo
+        s.dim = self.target.dim
+        s.n_vec, s.n_scal = self.n_vec, self.n_scal
+        s.vec = self.vec[lo].data_ptr()
+        s.scal = self.scal[lo].data_ptr()
+        s.ints = self.ints[lo].data_ptr()
+        s.seed = self.seed & ((1 << 64) - 1)
+        s.err_key = self.err_key.data_ptr()
+        return s
+
+    # reference-shaped views (host copies)
+    @property
+    def state_ids(self) -> list:
+        return self.ints[:, _lib.I_STATE].tolist()
+
+    @property
+    def sample_counts(self) -> list:
+        return self.ints[:, _lib.I_COUNT].tolist()
+
+    @property
+    def locals(self) -> list:
+        return [ChainView(self, j) for j in range(self.m)]
+
+    def chain(self, j: int) -> ChainView:
+        return ChainView(self, j)
+
+    def chain_position(self, j: int) -> np.ndarray:
+        return self.vec[j, 0].cpu().numpy()
+
+    def chain_key(self, j: int) -> RngKey:
+        row = self.ints[j].tolist()
+        return RngKey(self.seed & ((1 << 64) - 1), row[_lib.I_STREAM] & ((1 << 64) - 1),
+                      row[_lib.I_COUNTER] & ((1 << 64) - 1))
+
+    def first_error(self):
+        key = int(self.err_key.item()) & ((1 << 64) - 1)
+        if key == (1 << 64) - 1:
+            return None
+        j = key & ((1 << 24) - 1)
+        row = self.ints[j].tolist()
+        return (j, row[_lib.I_ERR_KIND], row[_lib.I_ERR_LABEL], row[_lib.I_ERR_TICK],
+                row[_lib.I_ERR_ITER])
+
+    def _step_one(self, j: int, k: int, variant: int, order) -> StepOutcome:
+        """One executor call on chain j entering state k (fsm.step & co)."""
+        K = self.n_states
+        self.ints[j, _lib.I_STATE] = k
+        before = self.ints[j].clone()
+        tick = int(before[_lib.I_TICK])
+        st = self.struct(j, j + 1)
+        out = _lib.Outputs()
+        ordv = (ctypes.c_int32 * K)(*(order or default_bundled_order(self.bundle.fsm)))
+        self.err_key.fill_(-1)
+        _lib.check(_lib.lib().fsmc_run(ctypes.byref(self.kernel), ctypes.byref(self.target.struct()),
+                                       ctypes.byref(st), 0, variant, ordv, tick + 1, 1,
+                                       ctypes.byref(out), 0, _lib.stream_ptr()), "fsmc_run")
+        after = self.ints[j].tolist()
+        if after[_lib.I_ERR_KIND] != _lib.E_NONE:
+            raise _cause(self.bundle, after[_lib.I_ERR_KIND], after[_lib.I_ERR_LABEL])
+        b0 = before[_lib.I_BLOCKS:_lib.I_BLOCKS + K].tolist()
+        b1 = after[_lib.I_BLOCKS:_lib.I_BLOCKS + K]
+        seq = list(order or default_bundled_order(self.bundle.fsm)) if variant == 1 else [k]
+        executed = tuple(s for s in seq if b1[s - 1] > b0[s - 1])
+        did = after[_lib.I_SHARED] > int(before[_lib.I_SHARED])
+        return StepOutcome(after[_lib.I_STATE], ChainView(self, j), k == K, did, executed)
+
+
+def _cause(bundle, kind: int, label: int) -> Exception:
+    """Map a device error record to the reference's exception types."""
+    from .kernels.base import KernelError
+    labels = bundle.fsm.labels
+    if kind == _lib.E_ZERO_START:
+        return KernelError("starting point has zero density")
+    if kind == _lib.E_GRAD:
+        return KernelError("non-finite gradient")
+    if kind == _lib.E_INIT:
+        return BlockFailure("INIT", "log-density evaluated to a non-finite value (NaN or +inf)")
+    name = "shared log f" if label == 0 else labels[label - 1]
+    return BlockFailure(name, "log-density evaluated to a non-finite value (NaN or +inf)")
+
+
+def init_batch(bundle, target, m: int, seed: int, x0=None, init_jitter: float = 0.0,
+               *, parent_stream: int = 0, chain_offset: int = 0) -> ChainBatch:
+    """m chains with streams split(key(seed), .) (lockstep.py:175-206).
+
+    ``chain_offset`` selects chains [offset, offset + m) of a larger batch:
+    chain j's trajectory depends only on (seed, j, target), so shards built
+    this way reproduce the full batch exactly.
+    """
+    if m < 1:
+        raise ValueError(f"need m >= 1 chains, got {m}")
+    bundle.check_target(target)
+    d = target.dim
+    base = np.zeros(d) if x0 is None else np.asarray(x0, dtype=float)
+    if base.shape != (d,):
+        raise ValueError(f"x0 shape {base.shape} does not match dim {d}")
+    batch = ChainBatch(bundle, target, m, seed, parent_stream, chain_offset)
+    x0d = torch.as_tensor(base, device="cuda")
+    _lib.check(_lib.lib().fsmc_init(ctypes.byref(batch.kernel), ctypes.byref(target.struct()),
+                                    ctypes.byref(batch.struct()), parent_stream & ((1 << 64) - 1),
+                                    chain_offset, x0d.data_ptr(), float(init_jitter),
+                                    _lib.stream_ptr()), "fsmc_init")
+    err = batch.first_error()
+    if err is not None:
+        raise _cause(bundle, err[1], err[2])
+    return batch
+
+
+def _validate_run_args(batch: ChainBatch, n: int):
+    if n < 1:
+        raise ValueError(f"need n >= 1 samples, got {n}")
+    if bool((batch.ints[:, _lib.I_COUNT] != 0).any()):
+        raise ValueError("batch has already been run; build a fresh one")
+
+
+def _outputs(n, m, d, L, want_ticks, want_samples=True):
+    samples = torch.empty((n, m, d), dtype=torch.float64, device="cuda") if want_samples else None
+    loops = torch.zeros((L, n, m), dtype=torch.int32, device="cuda")
+    ticks = torch.zeros((n, m), dtype=torch.int32, device="cuda") if want_ticks else None
+    out = _lib.Outputs()
+    out.samples = _lib.ptr(samples)
+    out.loop_counts = loops.data_ptr()
+    out.sample_ticks = _lib.ptr(ticks)
+    return samples, loops, ticks, out
+
+
+def _convert(x, output):
+    if x is None:
+        return None
+    if output == "torch":
+        return x
+    return x.cpu().numpy()
+
+
+def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str = "plain",
+                    cost_params: CostParams | None = None, tick_budget: int | None = None,
+                    bundled_order: tuple | None = None, record_sample_ticks: bool = False,
+                    tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
+                    lanes: int = 0):
+    """Run every chain's machine until each holds n samples (lockstep.py:308-416).
+
+    ``surplus=False`` skips the reference's surplus ticks (steps of chains
+    that already hold n samples, discarded by the reference): samples and
+    every per-sample ledger field are unchanged, only the two aggregate
+    counters then stop at each chain's n-th sample.
+    """
+    _validate_run_args(batch, n)
+    bundle.check_target(target)
+    if step_variant not in STEP_VARIANTS:
+        raise ValueError(f"step_variant must be one of {STEP_VARIANTS}")
+    if output not in ("numpy", "torch"):
+        raise ValueError("output must be 'numpy' or 'torch'")
+    params = cost_params or bundle.default_costs
+    machine = bundle.fsm
+    K = machine.n_states
+    if len(params.block_costs) != K:
+        raise ValueError(f"{len(params.block_costs)} block costs for a {K}-state kernel")
+    order = tuple(bundled_order or default_bundled_order(machine))
+    if step_variant == "bundled":
+        validate_bundled_order(machine, order)
+    m, d = batch.m, target.dim
+    loop_states = bundle.loop_states
+    samples, loops, ticks_out, out = _outputs(n, m, d, len(loop_states), record_sample_ticks)
+    limit = (tick_budget // tick_chunk) * tick_chunk if tick_budget is not None else _NO_LIMIT
+    lib = _lib.lib()
+    kern, tgt = batch.kernel, target.struct()
+    ordv = (ctypes.c_int32 * K)(*order)
+    variant = _VARIANT_ID[step_variant]
+
+    def launch(mode, tick_limit):
+        _lib.check(lib.fsmc_run(ctypes.byref(kern), ctypes.byref(tgt), ctypes.byref(batch.struct()),
+                                n, variant, ordv, tick_limit, mode, ctypes.byref(out), lanes,
+                                _lib.stream_ptr()), "fsmc_run")
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    launch(0, limit)
+    info = batch.ints[:, [_lib.I_COUNT, _lib.I_TICK, _lib.I_ERR_KIND, _lib.I_ERR_TICK]].cpu()
+    counts, cticks, ekind, etick = (info[:, i] for i in range(4))
+    errored = ekind != _lib.E_NONE
+    all_done = bool((counts >= n).all())
+    if all_done:
+        tmax = int(cticks.max())
+        tick_count = -(-tmax // tick_chunk) * tick_chunk
+    else:
+        tick_count = limit
+    first_err = int(etick[errored].min()) if bool(errored.any()) else _NO_LIMIT
+    run_to = min(tick_count, first_err)
+    if run_to < _NO_LIMIT and (surplus or first_err < _NO_LIMIT) and int(cticks.min()) < run_to:
+        launch(1, run_to)
+    torch.cuda.synchronize()
+    walltime = time.perf_counter() - t0
+    batch.active_mask = [False] * m
+
+    err = batch.first_error()
+    if err is not None:
+        j, kind, label, etick_j, eiter = err
+        if etick_j <= tick_count:
+            raise KernelRunError(chain=j, iteration=eiter, cause=_cause(bundle, kind, label))
+    counts_now = batch.ints[:, _lib.I_COUNT].cpu()
+    n_done = n if all_done else int(counts_now.min())
+    ledger = _fsm_ledger(bundle, params, step_variant, batch, loops, ticks_out, n_done,
+                         tick_count if all_done else limit, walltime, output)
+    if not all_done:
+        raise TickBudgetExceeded(tick_budget, ledger, counts_now.tolist())
+    return _convert(samples, output), ledger
+
+
+def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks, walltime,
+                output) -> CostLedger:
+    """lockstep.py:419-451"""
+    K = bundle.fsm.n_states
+    loop_states = bundle.loop_states
+    loop_execs = {s: _convert(loops[i, :n_rows].to(torch.int64), output)
+                  for i, s in enumerate(loop_states)}
+    it = sum(loops[loop_states.index(s), :n_rows].to(torch.int64) for s in bundle.iter_states)
+    blocks = batch.ints[:, _lib.I_BLOCKS:_lib.I_BLOCKS + K].sum(0)
+    tc = params.tick_cost(variant)
+    st = None if ticks_out is None else _convert(ticks_out[:n_rows].to(torch.int64), output)
+    return CostLedger(
+        iter_counts=_convert(it, output), loop_exec_counts=loop_execs, tick_count=int(ticks),
+        block_exec_counts=_convert(blocks, output), charged_cost=ticks * tc, walltime=walltime,
+        regime=f"fsm-{variant}", tick_cost=tc,
+        shared_evals_per_tick=params.shared_evals_per_tick(variant),
+        native_shared_evals=int(batch.ints[:, _lib.I_SHARED].sum()), sample_ticks=st)
+
+
+def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
+                         cost_params: CostParams | None = None, *, output: str = "numpy",
+                         lanes: int = 0):
+    """Lock-step baseline: one monolithic sample per chain per iteration with
+    barrier semantics (lockstep.py:238-305), on the device."""
+    _validate_run_args(batch, n)
+    bundle.check_target(target)
+    params = cost_params or bundle.default_costs
+    fsm = bundle.fsm
+    K = fsm.n_states
+    loop_states = tuple(sorted(params.loop_states or fsm.loop_states))
+    if not set(loop_states) <= fsm.loop_states:
+        raise ValueError(f"cost loop_states {loop_states} are not loop states of the kernel")
+    full = params.full_block_costs()
+    if len(full) != K:
+        raise ValueError(f"{len(full)} block costs for a {K}-state kernel")
+    nonloop_cost = sum(c for s, c in zip(range(1, K + 1), full) if s not in loop_states)
+    m, d = batch.m, target.dim
+    rec = bundle.loop_states
+    samples, loops, _, out = _outputs(n, m, d, len(rec), False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _lib.check(_lib.lib().fsmc_lockstep_run(ctypes.byref(batch.kernel),
+                                            ctypes.byref(target.struct()),
+                                            ctypes.byref(batch.struct()), n, ctypes.byref(out),
+                                            lanes, _lib.stream_ptr()), "fsmc_lockstep_run")
+    torch.cuda.synchronize()
+    walltime = time.perf_counter() - t0
+    batch.active_mask = [False] * m
+    errs = batch.ints[:, [_lib.I_ERR_KIND, _lib.I_ERR_ITER]].cpu()
+    bad = (errs[:, 0] != _lib.E_NONE).nonzero().flatten().tolist()
+    if bad:
+        j = min(bad, key=lambda c: (int(errs[c, 1]), c))
+        row = batch.ints[j].tolist()
+        raise KernelRunError(chain=j, iteration=row[_lib.I_ERR_ITER],
+                             cause=_cause(bundle, row[_lib.I_ERR_KIND], row[_lib.I_ERR_LABEL]))
+    L64 = loops.to(torch.int64)
+    charged = float(n) * nonloop_cost
+    if loop_states:
+        mx = L64.max(dim=2).values.to(torch.float64).cpu().numpy()   # [L, n]
+        for s in loop_states:
+            charged += full[s - 1] * float(mx[rec.index(s)].sum())
+    loop_execs = {s: _convert(L64[i], output) for i, s in enumerate(rec)}
+    it = sum(L64[rec.index(s)] for s in bundle.iter_states)
+    blocks = batch.ints[:, _lib.I_BLOCKS:_lib.I_BLOCKS + K].sum(0)
+    ledger = CostLedger(iter_counts=_convert(it, output), loop_exec_counts=loop_execs,
+                        tick_count=n, block_exec_counts=_convert(blocks, output),
+                        charged_cost=charged, walltime=walltime, regime="standard")
+    return _convert(samples, output), ledger
+
+
+def collect_samples(buffers: Sequence[Sequence], flags=None, n: int | None = None) -> list:
+    """Filter per-chain trace buffers to their flagged entries (lockstep.py:501-526)."""
+    out = []
+    for j, buf in enumerate(buffers):
+        if flags is None:
+            vals = list(buf)
+        else:
+            fl = flags[j]
+            if len(fl) != len(buf):
+                raise ValueError(f"chain {j}: {len(fl)} flags for {len(buf)} buffered values")
+            vals = [v for v, f in zip(buf, fl) if f]
+        if n is not None:
+            if len(vals) < n:
+                raise ValueError(f"chain {j}: only {len(vals)} samples, need {n}")
+            vals = vals[:n]
+        out.append(np.asarray(vals))
+    return out

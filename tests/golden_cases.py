@@ -1,0 +1,97 @@
+"""The golden fixtures (tests/golden/*.npz, frozen from the live reference by
+tests/golden/make_golden.py) and how to rebuild each case's kernel and target
+for the oracle (oracle/) and for the device engine (paper_2503_17405_b200)."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+# name -> (variants, kernel spec, target spec)
+CASES = {
+    "drmh_mog10": (("plain", "bundled", "amortized", "standard"), ("drmh", 100, 0.1), ("mog", 10, 0.9, (-3.0, 0.0, 3.0))),
+    "drmh_funnel10": (("plain", "bundled", "standard"), ("drmh", 100, 0.1), ("funnel", 10)),
+    "drmh_std1": (("plain", "bundled", "standard"), ("drmh", 100, 0.1), ("gauss", np.zeros(1), np.eye(1))),
+    "drmh_gauss3": (("plain", "bundled", "standard"), ("drmh", 20, 0.7),
+                    ("gauss", np.array([0.5, -1.0, 2.0]),
+                     np.array([[1.0, 0, 0], [0.3, 0.8, 0], [-0.2, 0.1, 0.5]]))),
+    "ess_conj100": (("plain", "bundled", "amortized", "standard"), ("ess",), ("conjugate", 100)),
+    "ess_conj2": (("plain", "bundled", "standard"), ("ess",), ("conjugate", 2)),
+    "ess_gpc64": (("amortized", "bundled", "standard"), ("ess",), ("gpc", 64)),
+    "nuts_corr100": (("plain", "bundled", "standard"), ("nuts", 0.05, 10, 1000.0), ("equicorr", 100, 0.99)),
+    "nuts_mog10": (("plain", "bundled", "standard"), ("nuts", 0.2, 6, 1000.0), ("mog", 10, 0.9, (-3.0, 0.0, 3.0))),
+    "nuts_funnel5": (("plain", "bundled", "standard"), ("nuts", 0.3, 5, 50.0), ("funnel", 5)),
+    "nuts_std2": (("plain", "bundled", "standard"), ("nuts", 0.9, 4, 1000.0), ("gauss", np.zeros(2), np.eye(2))),
+}
+
+
+def oracle_kernel(spec):
+    from oracle import oracle as O
+    if spec[0] == "drmh":
+        return O.drmh(spec[1], spec[2])
+    if spec[0] == "ess":
+        return O.elliptical()
+    return O.nuts(spec[1], spec[2], spec[3])
+
+
+def oracle_target(spec):
+    from oracle import oracle as O
+    kind = spec[0]
+    if kind == "mog":
+        return O.mog(spec[1], spec[2], list(spec[3]))
+    if kind == "funnel":
+        return O.funnel(spec[1])
+    if kind == "gauss":
+        return O.gaussian(spec[1], spec[2])
+    if kind == "equicorr":
+        return O.gaussian(np.zeros(spec[1]), np.linalg.cholesky(O.equicorrelated_covariance(spec[1], spec[2])))
+    if kind == "conjugate":
+        return O.conjugate(spec[1])
+    if kind == "gpc":
+        g = load("ess_gpc64")
+        return O.logistic_fspace(g["L"], g["y"])
+    raise KeyError(kind)
+
+
+def device_kernel(spec):
+    import paper_2503_17405_b200 as fm
+    if spec[0] == "drmh":
+        return fm.drmh_kernel(spec[1], spec[2])
+    if spec[0] == "ess":
+        return fm.elliptical_kernel()
+    return fm.nuts_kernel(spec[1], spec[2], spec[3])
+
+
+def device_target(spec, structure="auto"):
+    import paper_2503_17405_b200 as fm
+    from paper_2503_17405_b200 import targets as T
+    kind = spec[0]
+    if kind == "mog":
+        return fm.correlated_mog_target(spec[1], spec[2], list(spec[3]))
+    if kind == "funnel":
+        return fm.funnel_target(spec[1])
+    if kind == "gauss":
+        return fm.gaussian_target(spec[1], spec[2], structure=structure)
+    if kind == "equicorr":
+        return fm.gaussian_target(np.zeros(spec[1]),
+                                  np.linalg.cholesky(fm.equicorrelated_covariance(spec[1], spec[2])),
+                                  structure=structure)
+    if kind == "conjugate":
+        return fm.conjugate_target(spec[1])
+    if kind == "gpc":
+        return T.gp_classification_target(spec[1])
+    raise KeyError(kind)
+
+
+def rel_err(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b)))) if a.size else 0.0
