@@ -3,10 +3,10 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 # --fmad=false: every fp64 multiply and add rounds once, as numpy does (parity);
 # the explicit fma() calls (glibc log restatement, dot products) still fuse.
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -Xptxas -v
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -Xptxas -v $(EXTRA)
 CSRC := paper_2503_17405_b200/csrc
-BUILD := build
-LIB := paper_2503_17405_b200/libfsmc.so
+BUILD ?= build
+LIB ?= paper_2503_17405_b200/libfsmc.so
 UNITS := fsmc fam_drmh fam_ess fam_nuts
 OBJS := $(addprefix $(BUILD)/,$(addsuffix .o,$(UNITS)))
 HDR := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/fsmc.h

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) target_eval_kernel(fsmc_target t, co
                                                                long long m, double* lp, double* grad) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = smem + (size_t)(threadIdx.x / G) * t.dim;
+  double* sm = group_scratch<G, E>(smem, t.dim);
   const int d = t.dim;
   const long long groups = (long long)gridDim.x * (kThreads / G);
   for (long long j = (long long)blockIdx.x * (kThreads / G) + threadIdx.x / G; j < m; j += groups) {
@@ -323,12 +323,11 @@ fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, d
   GE ge;
   if (!pick_config(FSMC_ESS, t->dim, 0, ge)) return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
   cudaStream_t cs = (cudaStream_t)stream_;
-  size_t sm = (size_t)(kThreads / ge.g) * t->dim * sizeof(double);
   long long groups = (m + kThreads / ge.g - 1) / (kThreads / ge.g);
   int blocks = (int)std::min<long long>(groups, 148LL * 8);
 #define X(GG, EE)                                                                           \
   if (ge.g == GG && ge.e == EE) {                                                           \
-    target_eval_kernel<GG, EE><<<blocks, kThreads, sm, cs>>>(*t, X, m, lp, grad);           \
+    target_eval_kernel<GG, EE><<<blocks, kThreads, smem_bytes<GG, EE>(t->dim), cs>>>(*t, X, m, lp, grad); \
     CUDA_TRY(cudaGetLastError());                                                         \
     return FSMC_OK;                                                                       \
   }

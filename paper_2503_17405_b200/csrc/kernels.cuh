@@ -18,6 +18,27 @@ namespace fsmc {
 
 constexpr int kThreads = 128;
 
+// dynamic shared memory: one cooperative-normal scratch per warp, then the
+// per-group dense-operator scratch (dim doubles per lane group)
+template <int G, int E>
+__device__ __forceinline__ double* warp_scratch(double* smem, int dim) {
+  return smem + (threadIdx.x >> 5) * normal_scratch_doubles<E>();
+}
+template <int G, int E>
+__device__ __forceinline__ double* group_scratch(double* smem, int dim) {
+  return smem + (kThreads / 32) * normal_scratch_doubles<E>() + (threadIdx.x / G) * dim;
+}
+template <int G, int E>
+inline size_t smem_bytes(int dim) {
+  return ((size_t)(kThreads / G) * dim + (size_t)(kThreads / 32) * normal_scratch_doubles<E>()) *
+         sizeof(double);
+}
+
+// registers: 4 resident blocks per SM for thread-per-chain configurations so
+// that a full batch of chains is co-resident (no second wave)
+template <int G>
+__host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : 1; }
+
 struct LaunchCtx {
   int num_sms;
   unsigned* words;  // [0] chain queue, [1] barrier count, [2] barrier generation, [3..4] flags
@@ -31,12 +52,14 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
   extern __shared__ double smem[];
   Grp<G> grp;
   const int gib = threadIdx.x / G;
-  double* sm = smem + (size_t)gib * p.t.dim;
+  double* sm = group_scratch<G, E>(smem, p.t.dim);
   const long long groups = (long long)gridDim.x * (kThreads / G);
   const int d = p.t.dim;
+  double* ws = warp_scratch<G, E>(smem, p.t.dim);
   for (long long j = (long long)blockIdx.x * (kThreads / G) + gib; j < p.st.m; j += groups) {
     Core c;
     memset(&c, 0, sizeof(c));
+    c.ws = ws;
     uint64_t stream = split_stream(parent_stream, (uint64_t)(chain_offset + j));  // prng.py:84-94
     c.hsc = hash_seed_stream(p.st.seed, stream);
     c.state = 1;
@@ -75,10 +98,11 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
 // with its state in registers.  No barrier anywhere: chains in different
 // states simply execute different blocks.
 template <template <int, int> class F, int G, int E>
-__global__ void __launch_bounds__(kThreads) fsm_run_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = smem + (size_t)(threadIdx.x / G) * p.t.dim;
+  double* sm = group_scratch<G, E>(smem, p.t.dim);
+  double* ws = warp_scratch<G, E>(smem, p.t.dim);
   while (true) {
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
@@ -86,6 +110,7 @@ __global__ void __launch_bounds__(kThreads) fsm_run_kernel(Params p) {
     if (j >= p.st.m) break;
     Core c;
     core_load(c, p, j);
+    c.ws = ws;
     if (c.err_kind != FSMC_E_NONE) continue;
     F<G, E> f;
     f.load(p, j, grp);
@@ -138,13 +163,15 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
   using FF = F<G, E>;
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = smem + (size_t)(threadIdx.x / G) * p.t.dim;
+  double* sm = group_scratch<G, E>(smem, p.t.dim);
   const long long j = p.wave_lo + (long long)blockIdx.x * (kThreads / G) + threadIdx.x / G;
   bool live = j < p.wave_hi;
   Core c;
+  c.ws = warp_scratch<G, E>(smem, p.t.dim);
   FF f;
   if (live) {
     core_load(c, p, j);
+    c.ws = warp_scratch<G, E>(smem, p.t.dim);
     f.load(p, j, grp);
     live = c.err_kind == FSMC_E_NONE;
   }
@@ -199,7 +226,7 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
 // ------------------------------------------------------------- launchers
 template <template <int, int> class F, int G, int E>
 struct Launch {
-  static size_t smem(const Params& p) { return (size_t)(kThreads / G) * p.t.dim * sizeof(double); }
+  static size_t smem(const Params& p) { return smem_bytes<G, E>(p.t.dim); }
   static cudaError_t init(const Params& p, uint64_t ps, long long off, const double* x0, double jit,
                           cudaStream_t s) {
     long long groups = (p.st.m + (kThreads / G) - 1) / (kThreads / G);

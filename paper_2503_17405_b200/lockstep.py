@@ -265,11 +265,14 @@ def init_batch(bundle, target, m: int, seed: int, x0=None, init_jitter: float = 
         raise ValueError(f"need m >= 1 chains, got {m}")
     bundle.check_target(target)
     d = target.dim
-    base = np.zeros(d) if x0 is None else np.asarray(x0, dtype=float)
-    if base.shape != (d,):
-        raise ValueError(f"x0 shape {base.shape} does not match dim {d}")
+    if isinstance(x0, torch.Tensor):
+        x0d = x0.to(device="cuda", dtype=torch.float64).contiguous()
+    else:
+        x0d = torch.as_tensor(np.zeros(d) if x0 is None else np.asarray(x0, dtype=float),
+                              device="cuda")
+    if tuple(x0d.shape) != (d,):
+        raise ValueError(f"x0 shape {tuple(x0d.shape)} does not match dim {d}")
     batch = ChainBatch(bundle, target, m, seed, parent_stream, chain_offset)
-    x0d = torch.as_tensor(base, device="cuda")
     _lib.check(_lib.lib().fsmc_init(ctypes.byref(batch.kernel), ctypes.byref(target.struct()),
                                     ctypes.byref(batch.struct()), parent_stream & ((1 << 64) - 1),
                                     chain_offset, x0d.data_ptr(), float(init_jitter),
@@ -310,7 +313,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     cost_params: CostParams | None = None, tick_budget: int | None = None,
                     bundled_order: tuple | None = None, record_sample_ticks: bool = False,
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
-                    lanes: int = 0):
+                    lanes: int = 0, _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
@@ -348,7 +351,12 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    if _timing is not None:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
     launch(0, limit)
+    if _timing is not None:
+        ev[1].record()
     info = batch.ints[:, [_lib.I_COUNT, _lib.I_TICK, _lib.I_ERR_KIND, _lib.I_ERR_TICK]].cpu()
     counts, cticks, ekind, etick = (info[:, i] for i in range(4))
     errored = ekind != _lib.E_NONE
@@ -364,6 +372,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         launch(1, run_to)
     torch.cuda.synchronize()
     walltime = time.perf_counter() - t0
+    if _timing is not None:
+        _timing["run_kernel_ms"] = ev[0].elapsed_time(ev[1])
     batch.active_mask = [False] * m
 
     err = batch.first_error()
