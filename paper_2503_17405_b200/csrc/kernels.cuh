@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
 // Every lane group pulls chains from a queue and runs each to completion
 // with its state in registers.  No barrier anywhere: chains in different
 // states simply execute different blocks.
-template <template <int, int> class F, int G, int E>
+template <template <int, int> class F, int G, int E, int TK>
 __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Para
     const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
 #pragma unroll 1
     while (c.count < n_stop && c.tick < p.tick_limit)
-      if (!tick<F<G, E>, G, E>(p, c, f, sm, j, grp)) { ok = false; break; }
+      if (!tick<F<G, E>, G, E, TK>(p, c, f, sm, j, grp)) { ok = false; break; }
     f.store(p, j, grp);
     if (grp.lane == 0) {
       core_store(c, p, j);
@@ -158,7 +158,7 @@ __device__ __forceinline__ bool grid_any(const Params& p, bool pred, unsigned& p
 // barrier across all chains of the wave, so a sample costs max over chains of
 // its loop count.  Written as a uniform program counter so the state body
 // (and its log-density evaluation) is instantiated once.
-template <template <int, int> class F, int G, int E>
+template <template <int, int> class F, int G, int E, int TK>
 __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
   using FF = F<G, E>;
   extern __shared__ double smem[];
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
       }
       if (live && s) {
         bool did = false;
-        if (!run_state<FF, G, E>(p, c, f, s, did, sm, grp)) live = false;
+        if (!run_state<FF, G, E, TK>(p, c, f, s, did, sm, grp)) live = false;
         count_block<FF>(c, s);
         if (did) c.shared++;
       }
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
 }
 
 // ------------------------------------------------------------- launchers
-template <template <int, int> class F, int G, int E>
+template <template <int, int> class F, int G, int E, int TK>
 struct Launch {
   static size_t smem(const Params& p) { return smem_bytes<G, E>(p.t.dim); }
   static cudaError_t init(const Params& p, uint64_t ps, long long off, const double* x0, double jit,
@@ -236,18 +236,18 @@ struct Launch {
   }
   static cudaError_t run(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_run_kernel<F, G, E>,
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_run_kernel<F, G, E, TK>,
                                                                   kThreads, smem(p));
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
     int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
-    fsm_run_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p);
+    fsm_run_kernel<F, G, E, TK><<<blocks, kThreads, smem(p), s>>>(p);
     return cudaGetLastError();
   }
   static cudaError_t lockstep(Params p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lockstep_kernel<F, G, E>,
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lockstep_kernel<F, G, E, TK>,
                                                                   kThreads, smem(p));
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorLaunchOutOfResources;
@@ -258,7 +258,7 @@ struct Launch {
       p.wave_hi = std::min<long long>(p.st.m, lo + cap);
       int blocks = (int)((p.wave_hi - lo + per_block - 1) / per_block);
       void* args[] = {&p};
-      e = cudaLaunchCooperativeKernel((const void*)lockstep_kernel<F, G, E>, dim3(blocks),
+      e = cudaLaunchCooperativeKernel((const void*)lockstep_kernel<F, G, E, TK>, dim3(blocks),
                                       dim3(kThreads), args, smem(p), s);
       if (e != cudaSuccess) return e;
     }
@@ -266,13 +266,13 @@ struct Launch {
   }
 };
 
-// op: 0 init, 1 run, 2 lock-step
-template <template <int, int> class F, int G, int E>
+// op: 0 init, 1 run, 2 lock-step.  TK: compile-time plugin (0 = run-time switch)
+template <template <int, int> class F, int G, int E, int TK = 0>
 cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, uint64_t ps,
                       long long off, const double* x0, double jit) {
-  if (op == 0) return Launch<F, G, E>::init(p, ps, off, x0, jit, s);
-  if (op == 1) return Launch<F, G, E>::run(p, lc, s);
-  return Launch<F, G, E>::lockstep(p, lc, s);
+  if (op == 0) return Launch<F, G, E, 0>::init(p, ps, off, x0, jit, s);
+  if (op == 1) return Launch<F, G, E, TK>::run(p, lc, s);
+  return Launch<F, G, E, TK>::lockstep(p, lc, s);
 }
 
 }  // namespace fsmc

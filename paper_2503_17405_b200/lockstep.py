@@ -291,9 +291,10 @@ def _validate_run_args(batch: ChainBatch, n: int):
 
 
 def _outputs(n, m, d, L, want_ticks, want_samples=True):
+    # every row < n of every chain is written by the kernel before it is read
     samples = torch.empty((n, m, d), dtype=torch.float64, device="cuda") if want_samples else None
-    loops = torch.zeros((L, n, m), dtype=torch.int32, device="cuda")
-    ticks = torch.zeros((n, m), dtype=torch.int32, device="cuda") if want_ticks else None
+    loops = torch.empty((L, n, m), dtype=torch.int32, device="cuda")
+    ticks = torch.empty((n, m), dtype=torch.int32, device="cuda") if want_ticks else None
     out = _lib.Outputs()
     out.samples = _lib.ptr(samples)
     out.loop_counts = loops.data_ptr()
@@ -307,6 +308,14 @@ def _convert(x, output):
     if output == "torch":
         return x
     return x.cpu().numpy()
+
+
+def _counts(x, output):
+    """Ledger count matrices: int64 numpy arrays (the reference's type) for
+    output="numpy"; int32 device tensors, unconverted, for output="torch"."""
+    if output == "torch":
+        return x
+    return x.cpu().numpy().astype(np.int64)
 
 
 def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str = "plain",
@@ -395,14 +404,14 @@ def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks,
     """lockstep.py:419-451"""
     K = bundle.fsm.n_states
     loop_states = bundle.loop_states
-    loop_execs = {s: _convert(loops[i, :n_rows].to(torch.int64), output)
-                  for i, s in enumerate(loop_states)}
-    it = sum(loops[loop_states.index(s), :n_rows].to(torch.int64) for s in bundle.iter_states)
+    loop_execs = {s: _counts(loops[i, :n_rows], output) for i, s in enumerate(loop_states)}
+    its = [loops[loop_states.index(s), :n_rows] for s in bundle.iter_states]
+    it = its[0] if len(its) == 1 else sum(t.to(torch.int64) for t in its)
     blocks = batch.ints[:, _lib.I_BLOCKS:_lib.I_BLOCKS + K].sum(0)
     tc = params.tick_cost(variant)
-    st = None if ticks_out is None else _convert(ticks_out[:n_rows].to(torch.int64), output)
+    st = None if ticks_out is None else _counts(ticks_out[:n_rows], output)
     return CostLedger(
-        iter_counts=_convert(it, output), loop_exec_counts=loop_execs, tick_count=int(ticks),
+        iter_counts=_counts(it, output), loop_exec_counts=loop_execs, tick_count=int(ticks),
         block_exec_counts=_convert(blocks, output), charged_cost=ticks * tc, walltime=walltime,
         regime=f"fsm-{variant}", tick_cost=tc,
         shared_evals_per_tick=params.shared_evals_per_tick(variant),
