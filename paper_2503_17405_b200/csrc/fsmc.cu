@@ -171,6 +171,7 @@ bool pick_config(int family, int dim, int lanes, GE& out) {
     if (family == FSMC_DRMH && dim <= 16) lanes = 1;
     else if (dim <= 4) lanes = 1;
     else if (family == FSMC_NUTS && dim <= 16) lanes = 4;
+    else if (family == FSMC_ESS && dim > 256) lanes = 128;
     else lanes = 32;
   }
   const GE* best = nullptr;
