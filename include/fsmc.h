@@ -49,7 +49,8 @@ enum {
   FSMC_T_FUNNEL = 5,         /* Neal's funnel (BASELINE config 2) */
   FSMC_T_NANBAND = 6,        /* fault injection: std normal, `b` once x[0] > `a` */
   FSMC_T_LOGISTIC = 7,       /* -sum log(1+exp(-y*x)): GP-classification latent (f-space) */
-  FSMC_T_FLAT = 8            /* log density 0 */
+  FSMC_T_FLAT = 8,           /* log density 0 */
+  FSMC_T_LOGREG = 9          /* Bayesian logistic regression, N(0, I) prior (BASELINE config 5) */
 };
 
 /* Gaussian-prior split for the elliptical kernel (targets.py:37-42) */
@@ -82,6 +83,8 @@ typedef struct fsmc_target {
   const double* mat2_t;         /* [dim*dim] GAUSS_DENSE: precision^T row-major */
   const double* yvec;           /* [dim] LOGISTIC labels (+-1) */
   const double* prior_t;        /* [dim*dim] PRIOR_DENSE: L^T row-major (L lower-triangular) */
+  const double* data;           /* [n_rows*dim] LOGREG design matrix, row-major (labels in yvec) */
+  int64_t n_rows;
 } fsmc_target;
 
 /* Per-chain structure-of-arrays state, allocated by the caller with the
@@ -111,7 +114,8 @@ enum {
   FSMC_I_COUNTER = 0, FSMC_I_STREAM = 1, FSMC_I_STATE = 2, FSMC_I_TICK = 3, FSMC_I_COUNT = 4,
   FSMC_I_ERR_KIND = 5, FSMC_I_ERR_LABEL = 6, FSMC_I_ERR_TICK = 7, FSMC_I_ERR_ITER = 8,
   FSMC_I_SHARED = 9, FSMC_I_BLOCKS = 10 /* 6 slots */, FSMC_I_PEND = 16 /* 3 slots */,
-  FSMC_I_FAMILY = 19 /* family-private slots 19..31 */
+  FSMC_I_FAMILY = 19 /* family-private slots 19..30 */,
+  FSMC_I_RESUME = 31 /* batched mode: suspended-at-evaluation record */
 };
 /* error kinds in FSMC_I_ERR_KIND */
 enum { FSMC_E_NONE = 0, FSMC_E_BLOCK = 1, FSMC_E_ZERO_START = 2, FSMC_E_GRAD = 3, FSMC_E_INIT = 4 };
@@ -154,9 +158,28 @@ fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
                               int64_t n, const fsmc_outputs* out, int32_t lanes, void* stream_);
 
 /* Batched plugin evaluation: lp[j] = log p(X[j]), grad[j] (if non-NULL) for
- * rows X[m][dim] (TargetModel.log_density / log_density_and_grad). */
+ * rows X[m][dim] (TargetModel.log_density / log_density_and_grad).  family /
+ * lanes select the lane-group layout (0 = defaults) so a batched evaluation
+ * reduces in the same order as the sampling kernel. */
 fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, double* lp,
-                             double* grad, void* stream_);
+                             double* grad, int32_t family, int32_t lanes, void* stream_);
+
+/* Batched-evaluation mode (the paper's amortized step, fsm.py:252-273, made
+ * literal for dense targets).  Every chain advances, with no barrier, until
+ * its next log-density request (or until it holds n samples / reaches
+ * tick_limit, as in fsmc_run modes 0 / 1).  Each requesting chain appends
+ * itself to a compact list: req_chain[k] = j and theta[k][:] = the point to
+ * evaluate, k = atomicAdd(req_count, 1).  The caller evaluates every listed
+ * point in ONE batched call (e.g. GEMMs across chains), writes lp[k] (and
+ * grad[k][:] for gradient kernels), and calls fsmc_advance again: each chain
+ * first consumes its result, then runs on to its next request.  Repeat until
+ * *req_count == 0.  Samples, ticks and ledger rows are identical to fsmc_run.
+ * Buffers: theta/grad [m][dim], lp [m], req_chain [m] int32, req_count [1]. */
+fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                         int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                         const fsmc_outputs* out, const double* lp, const double* grad,
+                         double* theta, int32_t* req_chain, int32_t* req_count, int32_t lanes,
+                         void* stream_);
 
 /* Cross-chain diagnostic partials for effective_sample_size / R-hat
  * (analysis.py:336-418).  samples [n][m][dim]; uses rows burn..n-1.

@@ -241,6 +241,26 @@ static double target_eval(const or_target* t, const double* x, double* g, double
       if (x[0] > t->p0) return t->p1;
       return -0.5 * dot(x, x, d) - 0.5 * d * LOG_2PI;
     }
+    case OR_T_LOGREG: {
+      /* sum(y z - logaddexp(0, z)) - theta.theta/2; grad X^T (y - sigmoid(z)) - theta */
+      const int64_t N = t->n_rows;
+      double s = 0.0;
+      if (g)
+        for (int k = 0; k < d; k++) g[k] = 0.0;
+      for (int64_t i = 0; i < N; i++) {
+        const double* xi = t->data + (size_t)i * d;
+        double z = dot(xi, x, d);
+        double yi = t->yvec[i];
+        s += yi * z - np_logaddexp(0.0, z);
+        if (g) {
+          double r = yi - 1.0 / (1.0 + exp(-z));
+          for (int k = 0; k < d; k++) g[k] += xi[k] * r;
+        }
+      }
+      if (g)
+        for (int k = 0; k < d; k++) g[k] = g[k] - x[k];
+      return s - 0.5 * dot(x, x, d);
+    }
     case OR_T_LOGISTIC: {
       double s = 0.0;
       for (int i = 0; i < d; i++) s += np_logaddexp(0.0, -t->yvec[i] * x[i]);

@@ -28,7 +28,8 @@ enum {
   OR_T_FUNNEL = 3,    /* Neal's funnel (new; make_golden.py funnel_target) */
   OR_T_NANBAND = 4,   /* fault-injection standard normal (make_golden.py) */
   OR_T_LOGISTIC = 5,  /* -sum logaddexp(0, -y*x)  (GP-classification f-space) */
-  OR_T_FLAT = 6       /* log_density = 0 */
+  OR_T_FLAT = 6,      /* log_density = 0 */
+  OR_T_LOGREG = 7     /* Bayesian logistic regression, N(0, I) prior (make_golden.py logreg_target) */
 };
 
 typedef struct or_target {
@@ -47,6 +48,8 @@ typedef struct or_target {
   const double* prior_chol;   /* [d*d] lower-triangular, or NULL */
   int32_t prior_identity;     /* np.array_equal(L, eye(d)) */
   int32_t pad1;
+  const double* data;         /* [n_rows*d] row-major design matrix (logreg), labels in yvec */
+  int64_t n_rows;
 } or_target;
 
 typedef struct or_kernel {

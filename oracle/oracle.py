@@ -28,7 +28,7 @@ LOG_2PI = math.log(2.0 * math.pi)
 
 DRMH, ESS, NUTS = 1, 2, 3
 VARIANTS = {"plain": 0, "bundled": 1, "amortized": 2}
-T_GAUSS, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT = 1, 2, 3, 4, 5, 6
+T_GAUSS, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, T_LOGREG = 1, 2, 3, 4, 5, 6, 7
 
 
 def build(force: bool = False) -> str:
@@ -47,7 +47,8 @@ class _Target(ctypes.Structure):
                 ("pad0", ctypes.c_int32), ("log_norm", ctypes.c_double),
                 ("p0", ctypes.c_double), ("p1", ctypes.c_double),
                 ("mean", _P), ("L_inv", _P), ("prec", _P), ("modes", _P), ("yvec", _P),
-                ("prior_chol", _P), ("prior_identity", ctypes.c_int32), ("pad1", ctypes.c_int32)]
+                ("prior_chol", _P), ("prior_identity", ctypes.c_int32), ("pad1", ctypes.c_int32),
+                ("data", _P), ("n_rows", ctypes.c_int64)]
 
 
 class _Kernel(ctypes.Structure):
@@ -123,9 +124,11 @@ class OracleTarget:
         a = self.arrays
         t = _Target(kind=self.kind, dim=self.dim, n_modes=self.n_modes, log_norm=self.log_norm,
                     p0=self.p0, p1=self.p1, prior_identity=int(self.prior_identity))
-        for name in ("mean", "L_inv", "prec", "modes", "yvec", "prior_chol"):
+        for name in ("mean", "L_inv", "prec", "modes", "yvec", "prior_chol", "data"):
             if a.get(name) is not None:
                 setattr(t, name, _ptr(a[name]))
+        if a.get("data") is not None:
+            t.n_rows = a["data"].shape[0]
         return t
 
     def log_density(self, x):
@@ -191,6 +194,13 @@ def nanband(d, threshold, value) -> OracleTarget:
 
 def flat(d) -> OracleTarget:
     return OracleTarget(T_FLAT, d)
+
+
+def logreg(X, y) -> OracleTarget:
+    """Bayesian logistic regression, N(0, I) prior (tests/golden/make_golden.py logreg_target)."""
+    X = np.ascontiguousarray(np.asarray(X, dtype=float))
+    y = np.ascontiguousarray(np.asarray(y, dtype=float))
+    return OracleTarget(T_LOGREG, X.shape[1], arrays={"data": X, "yvec": y})
 
 
 def with_prior(residual: OracleTarget, chol) -> OracleTarget:

@@ -21,13 +21,14 @@ MAX_MODES = 8
 # families / variants / targets / priors (fsmc.h)
 DRMH, ESS, NUTS = 1, 2, 3
 PLAIN, BUNDLED, AMORTIZED = 0, 1, 2
-T_GAUSS_DIAG, T_GAUSS_DENSE, T_GAUSS_EQUICORR, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT = range(1, 9)
+T_GAUSS_DIAG, T_GAUSS_DENSE, T_GAUSS_EQUICORR, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, \
+    T_LOGREG = range(1, 10)
 PRIOR_NONE, PRIOR_IDENTITY, PRIOR_DENSE = 0, 1, 2
 
 # per-chain int slots
 I_COUNTER, I_STREAM, I_STATE, I_TICK, I_COUNT = 0, 1, 2, 3, 4
 I_ERR_KIND, I_ERR_LABEL, I_ERR_TICK, I_ERR_ITER = 5, 6, 7, 8
-I_SHARED, I_BLOCKS, I_PEND, I_FAMILY = 9, 10, 16, 19
+I_SHARED, I_BLOCKS, I_PEND, I_FAMILY, I_RESUME = 9, 10, 16, 19, 31
 E_NONE, E_BLOCK, E_ZERO_START, E_GRAD, E_INIT = 0, 1, 2, 3, 4
 
 _D = ctypes.c_double
@@ -52,7 +53,8 @@ class Target(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("dim", ctypes.c_int32), ("n_modes", ctypes.c_int32),
                 ("prior_kind", ctypes.c_int32), ("log_norm", _D), ("a", _D), ("b", _D),
                 ("pad", _D), ("offsets", _D * MAX_MODES), ("mean", _P), ("diag", _P),
-                ("diag2", _P), ("mat_t", _P), ("mat2_t", _P), ("yvec", _P), ("prior_t", _P)]
+                ("diag2", _P), ("mat_t", _P), ("mat2_t", _P), ("yvec", _P), ("prior_t", _P),
+                ("data", _P), ("n_rows", ctypes.c_int64)]
 
 
 class State(ctypes.Structure):
@@ -97,12 +99,18 @@ def lib():
                            ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                            ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Outputs),
                            ctypes.c_int32, _P]
+    L.fsmc_advance.restype = S
+    L.fsmc_advance.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target), ctypes.POINTER(State),
+                               ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                               ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Outputs),
+                               _P, _P, _P, _P, _P, ctypes.c_int32, _P]
     L.fsmc_lockstep_run.restype = S
     L.fsmc_lockstep_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                     ctypes.POINTER(State), ctypes.c_int64,
                                     ctypes.POINTER(Outputs), ctypes.c_int32, _P]
     L.fsmc_target_eval.restype = S
-    L.fsmc_target_eval.argtypes = [ctypes.POINTER(Target), _P, ctypes.c_int64, _P, _P, _P]
+    L.fsmc_target_eval.argtypes = [ctypes.POINTER(Target), _P, ctypes.c_int64, _P, _P,
+                                   ctypes.c_int32, ctypes.c_int32, _P]
     L.fsmc_diag_partials.restype = S
     L.fsmc_diag_partials.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]

@@ -13,3 +13,8 @@
 #define FSMC_DRMH_SPECIAL(X) X(1, 10, FSMC_T_MOG) X(1, 10, FSMC_T_FUNNEL)
 #define FSMC_ESS_SPECIAL(X) X(32, 4, FSMC_T_GAUSS_DIAG) X(128, 8, FSMC_T_LOGISTIC)
 #define FSMC_NUTS_SPECIAL(X) X(32, 4, FSMC_T_GAUSS_EQUICORR)
+
+// target_eval_kernel (fsmc_target_eval) is compiled for every (G, E) a family
+// uses, so the batched device evaluator reduces in the run kernel's order
+#define FSMC_EVAL_CONFIGS(X) X(1, 1) X(1, 2) X(1, 4) X(1, 10) X(1, 16) X(2, 2) X(2, 5) X(4, 3) \
+  X(4, 4) X(8, 2) X(32, 1) X(32, 2) X(32, 4) X(32, 8) X(128, 8)

@@ -295,6 +295,41 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
   return FSMC_OK;
 }
 
+fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                         int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                         const fsmc_outputs* out, const double* lp, const double* grad, double* theta,
+                         int32_t* req_chain, int32_t* req_count, int32_t lanes, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (!theta || !req_chain || !req_count || !lp || (k->family == FSMC_NUTS && !grad))
+    return fail(FSMC_ERR_ARG, "advance needs theta, req_chain, req_count, lp (and grad for NUTS)");
+  if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
+  GE ge;
+  if (!pick_config(k->family, t->dim, lanes, ge))
+    return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  if (out) p.out = *out;
+  p.n = n;
+  p.tick_limit = tick_limit;
+  p.variant = variant;
+  p.mode = mode;
+  int K = k->family == FSMC_NUTS ? 5 : 3;
+  for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
+  p.b_lp = lp;
+  p.b_grad = grad;
+  p.b_theta = theta;
+  p.b_req_chain = req_chain;
+  p.b_req_count = req_count;
+  cudaStream_t cs = (cudaStream_t)stream_;
+  p.next_chain = scratch().words;
+  CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
+  CUDA_TRY(cudaMemsetAsync(req_count, 0, sizeof(int32_t), cs));
+  CUDA_TRY(dispatch_family(3, ge, p, cs));
+  return FSMC_OK;
+}
+
 fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                               const fsmc_outputs* out, int32_t lanes, void* stream_) {
   fsmc_status s = check_args(k, t, st);
@@ -318,11 +353,12 @@ fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
 }
 
 fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, double* lp, double* grad,
-                             void* stream_) {
+                             int32_t family, int32_t lanes, void* stream_) {
   if (!t || !X || !lp || m < 0) return fail(FSMC_ERR_ARG, "bad target_eval args");
   if (!m) return FSMC_OK;
   GE ge;
-  if (!pick_config(FSMC_ESS, t->dim, 0, ge)) return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+  if (!pick_config(family ? family : FSMC_ESS, t->dim, lanes, ge))
+    return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
   cudaStream_t cs = (cudaStream_t)stream_;
   long long groups = (m + kThreads / ge.g - 1) / (kThreads / ge.g);
   int blocks = (int)std::min<long long>(groups, 148LL * 8);
@@ -332,7 +368,7 @@ fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, d
     CUDA_TRY(cudaGetLastError());                                                         \
     return FSMC_OK;                                                                       \
   }
-  FSMC_ESS_CONFIGS(X)
+  FSMC_EVAL_CONFIGS(X)
 #undef X
   return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
 }

@@ -127,6 +127,38 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Para
   }
 }
 
+// ------------------------------------------------------------- advance
+// Batched-evaluation mode: every chain runs to its next log-density request
+// and parks the point in the compact request list (see fsmc_advance).
+template <template <int, int> class F, int G, int E>
+__global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_advance_kernel(Params p) {
+  extern __shared__ double smem[];
+  Grp<G> grp;
+  double* sm = group_scratch<G, E>(smem, p.t.dim);
+  double* ws = warp_scratch<G, E>(smem, p.t.dim);
+  while (true) {
+    long long j = 0;
+    if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
+    j = grp.bcast_ll(j, 0);
+    if (j >= p.st.m) break;
+    Core c;
+    core_load(c, p, j);
+    c.ws = ws;
+    if (c.err_kind != FSMC_E_NONE) continue;
+    F<G, E> f;
+    f.load(p, j, grp);
+    long long resume = p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_RESUME];
+    bool ok = true;
+    advance_chain<F<G, E>, G, E>(p, c, f, sm, j, grp, resume, ok);
+    f.store(p, j, grp);
+    if (grp.lane == 0) {
+      core_store(c, p, j);
+      p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_RESUME] = resume;
+      if (!ok) report_error(c, p, j);
+    }
+  }
+}
+
 // ------------------------------------------------------------ lock-step
 // Grid-wide "any" + barrier.  Every thread of the (cooperatively launched,
 // hence co-resident) grid calls it the same number of times.
@@ -245,6 +277,17 @@ struct Launch {
     fsm_run_kernel<F, G, E, TK><<<blocks, kThreads, smem(p), s>>>(p);
     return cudaGetLastError();
   }
+  static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_advance_kernel<F, G, E>,
+                                                                  kThreads, smem(p));
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
+    int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
+    fsm_advance_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p);
+    return cudaGetLastError();
+  }
   static cudaError_t lockstep(Params p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lockstep_kernel<F, G, E, TK>,
@@ -272,6 +315,7 @@ cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, ui
                       long long off, const double* x0, double jit) {
   if (op == 0) return Launch<F, G, E, 0>::init(p, ps, off, x0, jit, s);
   if (op == 1) return Launch<F, G, E, TK>::run(p, lc, s);
+  if (op == 3) return Launch<F, G, E, 0>::advance(p, lc, s);
   return Launch<F, G, E, TK>::lockstep(p, lc, s);
 }
 

@@ -322,13 +322,21 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     cost_params: CostParams | None = None, tick_budget: int | None = None,
                     bundled_order: tuple | None = None, record_sample_ticks: bool = False,
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
-                    lanes: int = 0, _timing: dict | None = None):
+                    lanes: int = 0, evaluator=None, _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
     that already hold n samples, discarded by the reference): samples and
     every per-sample ledger field are unchanged, only the two aggregate
     counters then stop at each chain's n-th sample.
+
+    ``evaluator``: batched-evaluation mode.  Chains advance to their next
+    log-density request (``fsmc_advance``); all requests of a round are then
+    evaluated in one call ``evaluator(theta[k, d], lp[k], grad[k, d] | None)``
+    -- e.g. GEMMs across chains for a dense target -- and the chains resume.
+    ``evaluator="device"`` uses the per-point device plugin (bit-identical
+    to the default mode).  Targets whose ``batched_evaluator()`` is not None
+    (large dense designs) use it automatically.
     """
     _validate_run_args(batch, n)
     bundle.check_target(target)
@@ -353,10 +361,15 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     ordv = (ctypes.c_int32 * K)(*order)
     variant = _VARIANT_ID[step_variant]
 
-    def launch(mode, tick_limit):
-        _lib.check(lib.fsmc_run(ctypes.byref(kern), ctypes.byref(tgt), ctypes.byref(batch.struct()),
-                                n, variant, ordv, tick_limit, mode, ctypes.byref(out), lanes,
-                                _lib.stream_ptr()), "fsmc_run")
+    if evaluator is None and hasattr(target, "batched_evaluator"):
+        evaluator = target.batched_evaluator()
+    if evaluator is None:
+        def launch(mode, tick_limit):
+            _lib.check(lib.fsmc_run(ctypes.byref(kern), ctypes.byref(tgt),
+                                    ctypes.byref(batch.struct()), n, variant, ordv, tick_limit, mode,
+                                    ctypes.byref(out), lanes, _lib.stream_ptr()), "fsmc_run")
+    else:
+        launch = _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evaluator)
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -394,9 +407,58 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     n_done = n if all_done else int(counts_now.min())
     ledger = _fsm_ledger(bundle, params, step_variant, batch, loops, ticks_out, n_done,
                          tick_count if all_done else limit, walltime, output)
+    if hasattr(launch, "stats"):
+        ledger.extras.update(launch.stats)
     if not all_done:
         raise TickBudgetExceeded(tick_budget, ledger, counts_now.tolist())
     return _convert(samples, output), ledger
+
+
+def _device_evaluator(target, family: int, lanes: int):
+    """Per-point device plugin over the request list (fsmc_target_eval), in
+    the sampling kernel's lane layout (same reduction order)."""
+    tgt = target.struct()
+
+    def evaluate(theta, lp, g):
+        k = theta.shape[0]
+        _lib.check(_lib.lib().fsmc_target_eval(ctypes.byref(tgt), theta.data_ptr(), k, lp.data_ptr(),
+                                               _lib.ptr(g), family, lanes, _lib.stream_ptr()),
+                   "fsmc_target_eval")
+    return evaluate
+
+
+def _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evaluator):
+    """Rounds of fsmc_advance + one batched evaluation of every request."""
+    m, d = batch.m, target.dim
+    grad = bundle.family == _lib.NUTS
+    if evaluator == "device":
+        evaluator = _device_evaluator(target, bundle.family, lanes)
+    theta = torch.empty((m, d), dtype=torch.float64, device="cuda")
+    lp = torch.empty(m, dtype=torch.float64, device="cuda")
+    g = torch.empty((m, d), dtype=torch.float64, device="cuda") if grad else None
+    req_chain = torch.empty(m, dtype=torch.int32, device="cuda")
+    req_count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib = _lib.lib()
+    kern, tgt = batch.kernel, target.struct()
+    stats = {"rounds": 0, "evaluations": 0}
+
+    def launch(mode, tick_limit):
+        while True:
+            _lib.check(lib.fsmc_advance(ctypes.byref(kern), ctypes.byref(tgt),
+                                        ctypes.byref(batch.struct()), n, variant, ordv, tick_limit,
+                                        mode, ctypes.byref(out), lp.data_ptr(), _lib.ptr(g),
+                                        theta.data_ptr(), req_chain.data_ptr(),
+                                        req_count.data_ptr(), lanes, _lib.stream_ptr()),
+                       "fsmc_advance")
+            k = int(req_count.item())
+            if k == 0:
+                return
+            stats["rounds"] += 1
+            stats["evaluations"] += k
+            evaluator(theta[:k], lp[:k], None if g is None else g[:k])
+
+    launch.stats = stats
+    return launch
 
 
 def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks, walltime,

@@ -28,6 +28,7 @@ __all__ = [
     "standard_normal_target", "equicorrelated_covariance", "equicorrelated_gaussian_target",
     "correlated_mog_target", "funnel_target", "gp_classification_data",
     "gp_classification_target", "logistic_residual", "nan_band_target", "flat_target",
+    "logistic_regression_data", "logistic_regression_target",
     "conjugate_target",
 ]
 
@@ -96,9 +97,11 @@ class TargetModel:
         t.b = self.b
         for i, o in enumerate(self.offsets):
             t.offsets[i] = o
-        for name in ("mean", "diag", "diag2", "mat_t", "mat2_t", "yvec"):
+        for name in ("mean", "diag", "diag2", "mat_t", "mat2_t", "yvec", "data"):
             if name in dev:
                 setattr(t, name, dev[name].data_ptr())
+        if "data" in self.arrays:
+            t.n_rows = int(self.arrays["data"].shape[0])
         t.prior_kind = _lib.PRIOR_NONE
         if self.gaussian_prior is not None:
             L = np.asarray(self.gaussian_prior.chol, dtype=float)
@@ -119,7 +122,8 @@ class TargetModel:
         g = torch.empty_like(X) if grad else None
         t = self.struct()
         _lib.check(_lib.lib().fsmc_target_eval(ctypes.byref(t), X.data_ptr(), m, lp.data_ptr(),
-                                               _lib.ptr(g), _lib.stream_ptr()), "fsmc_target_eval")
+                                               _lib.ptr(g), 0, 0, _lib.stream_ptr()),
+                   "fsmc_target_eval")
         return lp, g
 
     def log_density(self, x) -> float:
@@ -287,6 +291,28 @@ def conjugate_target(dim=2, rho=0.3, lik_mu=0.5, lik_var=0.5) -> TargetModel:
     prior_cov = equicorrelated_covariance(dim, rho)
     lik = gaussian_target(np.full(dim, lik_mu), np.linalg.cholesky(lik_var * np.eye(dim)))
     return _with_prior(lik, np.linalg.cholesky(prior_cov), "conjugate")
+
+
+def logistic_regression_data(n_obs: int = 100_000, d: int = 256, seed: int = 0):
+    """Synthetic Bayesian logistic regression (BASELINE config 5; SURVEY.md
+    Appendix B): X ~ N(0,1)/sqrt(d), theta* ~ N(0, I), y ~ Bernoulli(sigmoid(X theta*))."""
+    rng = np.random.default_rng(seed)
+    X = rng.normal(size=(n_obs, d)) / math.sqrt(d)
+    theta = rng.normal(size=d)
+    y = (rng.uniform(size=n_obs) < 1.0 / (1.0 + np.exp(-(X @ theta)))).astype(float)
+    return X, y
+
+
+def logistic_regression_target(X, y) -> TargetModel:
+    """log p(theta) = sum_i [y_i z_i - log(1 + e^{z_i})] - theta.theta/2 with
+    z = X theta; gradient X^T (y - sigmoid(z)) - theta.  Restated for the
+    oracle in tests/golden/make_golden.py (logreg_target)."""
+    X = np.ascontiguousarray(np.asarray(X, dtype=float))
+    y = np.ascontiguousarray(np.asarray(y, dtype=float))
+    if X.ndim != 2 or y.shape != (X.shape[0],):
+        raise TargetError("need X [n, d] and y [n]")
+    return TargetModel(f"logreg-{X.shape[0]}x{X.shape[1]}", X.shape[1], _lib.T_LOGREG,
+                       arrays={"data": X, "yvec": y})
 
 
 def gp_classification_data(n_pts: int, seed: int = 20240617):

@@ -80,6 +80,33 @@ def gp_class_fspace_target(n_pts: int) -> TargetModel:
             chol=L, residual_log_density=lambda x: float(-np.logaddexp(0.0, -y * x).sum())))
 
 
+def logreg_data(n_obs: int, d: int, seed: int = 0):
+    """Synthetic Bayesian logistic regression:
+    X ~ N(0,1)/sqrt(d), theta* ~ N(0, I), y ~ Bernoulli(sigmoid(X theta*))."""
+    rng = np.random.default_rng(seed)
+    X = rng.normal(size=(n_obs, d)) / math.sqrt(d)
+    theta = rng.normal(size=d)
+    y = (rng.uniform(size=n_obs) < 1.0 / (1.0 + np.exp(-(X @ theta)))).astype(float)
+    return X, y
+
+
+def logreg_target(X, y) -> TargetModel:
+    """log p(theta) = sum_i [y_i z_i - log(1 + e^{z_i})] - theta.theta/2, z = X theta;
+    grad = X^T (y - sigmoid(z)) - theta."""
+    d = X.shape[1]
+
+    def lp_grad(theta):
+        theta = np.asarray(theta, dtype=float)
+        z = X @ theta
+        lp = float(np.sum(y * z - np.logaddexp(0.0, z))) - 0.5 * float(theta @ theta)
+        g = X.T @ (y - 1.0 / (1.0 + np.exp(-z))) - theta
+        return lp, g
+
+    return TargetModel(name=f"logreg-{X.shape[0]}x{d}", dim=d,
+                       log_density=lambda t: lp_grad(t)[0], gradient=lambda t: lp_grad(t)[1],
+                       log_density_and_grad=lp_grad)
+
+
 def nan_band_target(d: int, threshold: float, value: float) -> TargetModel:
     """Standard normal that returns ``value`` (NaN or +inf) once x[0] > threshold."""
     def lp(x):
@@ -214,7 +241,19 @@ def main():
              m=8, n=60, seed=7, variants=("plain", "bundled"))
     run_case("nuts_std2", nuts_kernel(0.9, 4), gaussian_target(np.zeros(2), np.eye(2)),
              m=8, n=100, seed=8, variants=("plain", "bundled"), tick_chunk=1)
+    X, y = logreg_data(512, 16, seed=0)
+    run_case("nuts_logreg512x16", nuts_kernel(0.1, 8), logreg_target(X, y),
+             m=6, n=40, seed=9, variants=("plain", "bundled"), extra={"X": X, "y": y})
+
+
+def main_logreg_only():
+    X, y = logreg_data(512, 16, seed=0)
+    run_case("nuts_logreg512x16", nuts_kernel(0.1, 8), logreg_target(X, y),
+             m=6, n=40, seed=9, variants=("plain", "bundled"), extra={"X": X, "y": y})
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "logreg":
+        main_logreg_only()
+    else:
+        main()

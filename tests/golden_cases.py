@@ -30,6 +30,7 @@ CASES = {
     "nuts_mog10": (("plain", "bundled", "standard"), ("nuts", 0.2, 6, 1000.0), ("mog", 10, 0.9, (-3.0, 0.0, 3.0))),
     "nuts_funnel5": (("plain", "bundled", "standard"), ("nuts", 0.3, 5, 50.0), ("funnel", 5)),
     "nuts_std2": (("plain", "bundled", "standard"), ("nuts", 0.9, 4, 1000.0), ("gauss", np.zeros(2), np.eye(2))),
+    "nuts_logreg512x16": (("plain", "bundled", "standard"), ("nuts", 0.1, 8, 1000.0), ("logreg",)),
 }
 
 
@@ -58,6 +59,9 @@ def oracle_target(spec):
     if kind == "gpc":
         g = load("ess_gpc64")
         return O.logistic_fspace(g["L"], g["y"])
+    if kind == "logreg":
+        g = load("nuts_logreg512x16")
+        return O.logreg(g["X"], g["y"])
     raise KeyError(kind)
 
 
@@ -88,6 +92,9 @@ def device_target(spec, structure="auto"):
         return fm.conjugate_target(spec[1])
     if kind == "gpc":
         return T.gp_classification_target(spec[1])
+    if kind == "logreg":
+        g = load("nuts_logreg512x16")
+        return T.logistic_regression_target(g["X"], g["y"])
     raise KeyError(kind)
 
 
