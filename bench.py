@@ -43,11 +43,32 @@ CONFIGS = {
                family="nuts", m=16384, n=1000, d=100, variant="bundled", m_cpu=16),
     "c4": dict(workload="C4: elliptical slice FSM, GP-classification latent d=1024 (f-space)",
                family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4),
+    "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
+                        "depth 10; batched TF32 gradient evaluation across chains",
+               family="nuts", m=131072, n=2, d=256, variant="bundled", m_cpu=16, n_obs=100_000,
+               batched="tf32"),
 }
+
+
+_LOGREG = {}
+
+
+def logreg_data(cfg):
+    key = (cfg["n_obs"], cfg["d"])
+    if key not in _LOGREG:
+        from paper_2503_17405_b200.targets import logistic_regression_data
+        _LOGREG[key] = logistic_regression_data(cfg["n_obs"], cfg["d"], seed=0)
+    return _LOGREG[key]
 
 
 def make_workload(cfg, fm=None, oracle=False):
     """Kernel + target of a config, for the engine or for the oracle."""
+    if cfg.get("n_obs"):
+        X, y = logreg_data(cfg)
+        if oracle:
+            from oracle import oracle as O
+            return O.nuts(0.01, 10), O.logreg(X, y)
+        return fm.nuts_kernel(0.01, 10), fm.targets.logistic_regression_target(X, y)
     if oracle:
         from oracle import oracle as O
         if cfg["family"] == "drmh":
@@ -199,11 +220,16 @@ def main():
     off = rank * m
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
+    evaluator = None
+    if cfg.get("batched"):
+        from paper_2503_17405_b200.dense import LogisticRegressionEvaluator
+        evaluator = LogisticRegressionEvaluator(*logreg_data(cfg), precision=cfg["batched"])
+
     def one_step(seed, timing=None):
         batch = fm.init_batch(bundle, target, m, seed, chain_offset=off)
         return fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
                                   output="torch", surplus=False, lanes=args.lanes,
-                                  _timing=timing)
+                                  evaluator=evaluator, _timing=timing)
 
     for s in range(args.warmup):
         one_step(1000 + s)
@@ -229,18 +255,22 @@ def main():
 
     # ESS / R-hat of the last step's samples: per-rank partials, all-reduced
     burn = n // 10
-    mom = analysis.diag_moments(samples, burn=burn)
-    if world > 1:
-        loc = distributed.LocalMoments(mom.n, analysis_chain_means(samples, burn),
-                                       mom.max_chain_var, mom.acov_tile)
-        mom = distributed.allreduce_moments(loc, device=dev)
-    ess = analysis.ess_from_moments(mom)
-    rh = analysis.rhat_from_moments(mom)
-    ess_per_sec = ess.pooled / (t_total / args.steps)
+    has_ess = n - burn >= 10
+    ess_pooled = ess_per_sec = rhat_max = None
+    if has_ess:
+        mom = analysis.diag_moments(samples, burn=burn)
+        if world > 1:
+            loc = distributed.LocalMoments(mom.n, analysis_chain_means(samples, burn),
+                                           mom.max_chain_var, mom.acov_tile)
+            mom = distributed.allreduce_moments(loc, device=dev)
+        ess = analysis.ess_from_moments(mom)
+        ess_pooled = ess.pooled
+        rhat_max = float(np.nanmax(analysis.rhat_from_moments(mom)))
+        ess_per_sec = ess.pooled / (t_total / args.steps)
 
     # lock-step (vmap-style) baseline, same code, same chains
     lock = None
-    if not args.no_lockstep:
+    if not args.no_lockstep and not cfg.get("batched"):
         lock_ms = []
         for s in range(2):
             flush.fill_(s)
@@ -266,9 +296,12 @@ def main():
         x0 = x0_host.to(dev, non_blocking=True)
         batch = fm.init_batch(bundle, target, m, 500 + s, x0=x0, chain_offset=off)
         smp, _ = fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
-                                    output="torch", surplus=False, lanes=args.lanes)
-        summ = fm.effective_sample_size(smp, burn=burn)
-        _ = summ.pooled
+                                    output="torch", surplus=False, lanes=args.lanes,
+                                    evaluator=evaluator)
+        if has_ess:
+            _ = fm.effective_sample_size(smp, burn=burn).pooled
+        else:
+            _ = smp.mean(dim=(0, 1)).cpu()
         barrier()
         e2e_s.append(time.perf_counter() - t0)
     t_e2e = max_over_ranks(min(e2e_s))
@@ -278,6 +311,7 @@ def main():
 
     # roofline of the dominant kernel (fsm_run_kernel): algorithmic HBM bytes
     kms = statistics.mean(kern_ms)
+    evals = ledger.extras.get("evaluations", 0)
     st_bytes = 2 * m * 8 * (ledger_state_words(bundle, d))
     out_bytes = n * m * d * 8 + n * m * 4 * len(bundle.loop_states)
     traffic_bytes = st_bytes + out_bytes
@@ -291,6 +325,17 @@ def main():
             "note": "state in registers for the whole run: HBM carries only samples and "
                     "ledger rows; the kernel is fp64/int issue-bound (see profiles/)"}
 
+    if cfg.get("batched"):
+        # dominant work: the two contractions per evaluation, 4 N d flops each
+        flops = 4.0 * cfg["n_obs"] * d * evals
+        ach = flops / (kms / 1e3) / 1e12
+        pk = peaks.get("bf16_tflops_sustained", 1395.2) / 2.0   # dense TF32 = half of bf16
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "frac": ach / pk, "traffic": None, "kernel": "batched logistic-regression "
+                "evaluation (cuBLAS TF32 GEMMs, interim) + fsm_advance_kernel<Nuts,128,2>",
+                "kernel_ms": kms, "algorithmic_flops": flops,
+                "note": "peak = half the measured sustained bf16 figure (dense TF32 rate); "
+                        "whole run (advance + evaluation) timed"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu, _ = cpu_baseline(cfg, steps=1, warmup=0)
@@ -305,10 +350,11 @@ def main():
                            "parallelism": f"chains sharded over {world} GPU(s), no data-path "
                                           "collective", "l2": "flushed between steps (256 MiB write)",
                            "surplus_ticks": "skipped (discarded by the reference)"},
-                "ess_per_sec": ess_per_sec, "ess_pooled": ess.pooled, "rhat_max": float(np.nanmax(rh)),
+                "ess_per_sec": ess_per_sec, "ess_pooled": ess_pooled, "rhat_max": rhat_max,
                 "lockstep": lock, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-                "clocks": clk, "gpu_launches": 2 * args.steps,
-                "tick_count": ledger.tick_count}
+                "clocks": clk, "gpu_launches": args.steps * (2 + (ledger.extras.get("rounds") or 0)),
+                "tick_count": ledger.tick_count,
+                "evaluations_per_step": evals, "rounds_per_step": ledger.extras.get("rounds")}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

@@ -181,6 +181,14 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
                          double* theta, int32_t* req_chain, int32_t* req_count, int32_t lanes,
                          void* stream_);
 
+/* Logistic-regression evaluation epilogue over a tile of chains: given
+ * Z [rows][N] = Theta X^T (fp32, from the contraction), labels y [N]:
+ *   lp[r]   += sum_i y_i z_ri - log(1 + e^{z_ri})     (fp64 accumulation)
+ *   R[r][i]  = y_i - sigmoid(z_ri)                    (fp32, in place over Z allowed)
+ * One pass over Z; the caller adds -theta.theta/2 and forms G = R X - Theta. */
+fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, int64_t N,
+                                 float* R, double* lp, void* stream_);
+
 /* Cross-chain diagnostic partials for effective_sample_size / R-hat
  * (analysis.py:336-418).  samples [n][m][dim]; uses rows burn..n-1.
  *   chain_mean [m][dim] (computed when lag0 == 0), acov [32][dim] = sum over chains of

@@ -111,6 +111,8 @@ def lib():
     L.fsmc_target_eval.restype = S
     L.fsmc_target_eval.argtypes = [ctypes.POINTER(Target), _P, ctypes.c_int64, _P, _P,
                                    ctypes.c_int32, ctypes.c_int32, _P]
+    L.fsmc_logreg_epilogue.restype = S
+    L.fsmc_logreg_epilogue.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]
     L.fsmc_diag_partials.restype = S
     L.fsmc_diag_partials.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]

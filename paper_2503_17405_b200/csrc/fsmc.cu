@@ -138,6 +138,38 @@ __global__ void diag_acov_kernel(const double* S, long long n, long long m, long
     if (lag0 + t < N) atomicAdd(&acov[t * d + k], acc[t] / (double)N);
 }
 
+// logistic-regression epilogue: one pass over Z [rows][N] (see fsmc.h)
+constexpr int kEpiCols = 8192;
+__global__ void __launch_bounds__(256) logreg_epilogue_kernel(const float* __restrict__ Z,
+                                                              const float* __restrict__ y,
+                                                              long long N, float* R, double* lp) {
+  const long long r = blockIdx.y;
+  const long long c0 = (long long)blockIdx.x * kEpiCols;
+  const long long c1 = c0 + kEpiCols < N ? c0 + kEpiCols : N;
+  const float* zr = Z + r * N;
+  float* rr = R + r * N;
+  double acc = 0.0;
+  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const float z = zr[i];
+    const float yi = __ldg(&y[i]);
+    const float e = expf(-fabsf(z));
+    const float sp = fmaxf(z, 0.0f) + log1pf(e);           // log(1 + e^z), stable
+    acc += (double)(yi * z - sp);
+    const float sig = z >= 0.0f ? 1.0f / (1.0f + e) : e / (1.0f + e);
+    rr[i] = yi - sig;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; w++) s += part[w];
+    atomicAdd(&lp[r], s);
+  }
+}
+
 // ================================================================ dispatch
 namespace fsmc {
 cudaError_t dispatch_drmh(int, int, int, Params&, const LaunchCtx&, cudaStream_t, uint64_t, long long,
@@ -172,6 +204,7 @@ bool pick_config(int family, int dim, int lanes, GE& out) {
     else if (dim <= 4) lanes = 1;
     else if (family == FSMC_NUTS && dim <= 16) lanes = 4;
     else if (family == FSMC_ESS && dim > 256) lanes = 128;
+    else if (family == FSMC_NUTS && dim > 128) lanes = 128;
     else lanes = 32;
   }
   const GE* best = nullptr;
@@ -371,6 +404,17 @@ fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, d
   FSMC_EVAL_CONFIGS(X)
 #undef X
   return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+}
+
+fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, int64_t N, float* R,
+                                 double* lp, void* stream_) {
+  if (!Z || !y || !R || !lp || rows < 0 || N < 1) return fail(FSMC_ERR_ARG, "bad epilogue args");
+  if (!rows) return FSMC_OK;
+  if (rows > 65535) return fail(FSMC_ERR_ARG, "at most 65535 rows per epilogue call");
+  dim3 grid((unsigned)((N + kEpiCols - 1) / kEpiCols), (unsigned)rows);
+  logreg_epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream_>>>(Z, y, N, R, lp);
+  CUDA_TRY(cudaGetLastError());
+  return FSMC_OK;
 }
 
 fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int64_t dim, int64_t burn,

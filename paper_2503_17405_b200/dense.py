@@ -2,8 +2,8 @@
 
 In batched-evaluation mode (``run_fsm_batched(..., evaluator=...)``) every
 chain advances to its next log-density request and all requests of a round
-are evaluated together, so a dense target becomes a pair of GEMMs across
-chains instead of one GEMV per chain (the paper's amortized step,
+are evaluated together, so a dense target becomes a pair of contractions
+across chains instead of one GEMV per chain (the paper's amortized step,
 ``fsm.py:252-273``).
 
 Bayesian logistic regression (``targets.logistic_regression_target``):
@@ -13,8 +13,9 @@ Bayesian logistic regression (``targets.logistic_regression_target``):
     G = (y − σ(Z)) X − Θ           [k, d]
 
 ``precision="fp64"`` evaluates in IEEE double (parity with the per-chain
-plugin to reduction order); ``"tf32"`` / ``"bf16"`` run the contractions on
-the tensor cores with fp32 accumulation (distributional parity only).
+plugin up to reduction order).  ``"tf32"`` runs both contractions on the
+tensor cores (fp32 accumulation) and the σ / softplus / row-sum epilogue in
+one pass over Z (``fsmc_logreg_epilogue``); distributional parity only.
 Chains are processed in tiles so Z never exceeds ``tile`` rows.
 """
 
@@ -22,41 +23,52 @@ from __future__ import annotations
 
 import torch
 
+from . import _lib
+
 __all__ = ["LogisticRegressionEvaluator"]
 
 
 class LogisticRegressionEvaluator:
     def __init__(self, X, y, precision: str = "fp64", tile: int = 4096):
-        if precision not in ("fp64", "tf32", "bf16", "fp32"):
-            raise ValueError("precision must be fp64, fp32, tf32 or bf16")
+        if precision not in ("fp64", "tf32"):
+            raise ValueError("precision must be fp64 or tf32")
         self.precision = precision
         self.tile = int(tile)
         X = torch.as_tensor(X, dtype=torch.float64, device="cuda").contiguous()
         y = torch.as_tensor(y, dtype=torch.float64, device="cuda").contiguous()
         if precision == "fp64":
             self.X, self.y = X, y
-        elif precision == "bf16":
-            self.X, self.y = X.to(torch.bfloat16), y.to(torch.float32)
         else:
             self.X, self.y = X.to(torch.float32), y.to(torch.float32)
+            self.XT = self.X.T.contiguous()
 
     def __call__(self, theta: torch.Tensor, lp: torch.Tensor, grad: torch.Tensor | None):
+        if self.precision == "fp64":
+            return self._fp64(theta, lp, grad)
         k = theta.shape[0]
         prev = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = self.precision == "tf32"
+        torch.backends.cuda.matmul.allow_tf32 = True
         try:
             for lo in range(0, k, self.tile):
                 hi = min(k, lo + self.tile)
                 th = theta[lo:hi]
-                tc = th.to(self.X.dtype)
-                z = tc @ self.X.T                                   # [t, N]
-                zf = z.to(self.y.dtype)
-                # numpy logaddexp(0, z) = max(z, 0) + log1p(exp(-|z|))
-                sp = torch.clamp_min(zf, 0) + torch.log1p(torch.exp(-zf.abs()))
-                lp[lo:hi] = ((self.y * zf - sp).sum(dim=1)).to(torch.float64) \
-                    - 0.5 * (th * th).sum(dim=1)
+                z = th.to(torch.float32) @ self.XT                      # [t, N] fp32
+                lp[lo:hi] = -0.5 * (th * th).sum(dim=1)
+                _lib.check(_lib.lib().fsmc_logreg_epilogue(
+                    z.data_ptr(), self.y.data_ptr(), hi - lo, z.shape[1], z.data_ptr(),
+                    lp[lo:hi].data_ptr(), _lib.stream_ptr()), "fsmc_logreg_epilogue")
                 if grad is not None:
-                    r = (self.y - torch.sigmoid(zf)).to(self.X.dtype)
-                    grad[lo:hi] = (r @ self.X).to(torch.float64) - th
+                    grad[lo:hi] = (z @ self.X).to(torch.float64) - th
         finally:
             torch.backends.cuda.matmul.allow_tf32 = prev
+
+    def _fp64(self, theta, lp, grad):
+        k = theta.shape[0]
+        for lo in range(0, k, self.tile):
+            hi = min(k, lo + self.tile)
+            th = theta[lo:hi]
+            z = th @ self.X.T
+            sp = torch.clamp_min(z, 0) + torch.log1p(torch.exp(-z.abs()))
+            lp[lo:hi] = (self.y * z - sp).sum(dim=1) - 0.5 * (th * th).sum(dim=1)
+            if grad is not None:
+                grad[lo:hi] = (self.y - torch.sigmoid(z)) @ self.X - th
