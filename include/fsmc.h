@@ -189,6 +189,19 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
 fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, int64_t N,
                                  float* R, double* lp, void* stream_);
 
+/* Fused tcgen05 evaluation of the logistic-regression target over k chains
+ * (BASELINE config 5; d must be 256):  per 128-chain tile, S = Theta X^T and
+ * G += (y - sigmoid(S)) X accumulate in TMEM (bf16 operands via TMA, fp32
+ * accumulation), the logits never reach HBM.  theta [k][256] fp64 in,
+ * lp [k] = sum_i y z - log(1+e^z) - theta.theta/2, grad [k][256] = G - theta.
+ * Scratch theta_bf16 holds ceil(k/128)*128 x 256 bf16; x_bf16 [n_obs][256]
+ * and xt_bf16 [256][n_obs] are the design matrix and its transpose in bf16
+ * (n_obs a multiple of 8). */
+fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16, const void* x_bf16,
+                                const void* xt_bf16, const float* y, int64_t n_obs, int64_t dim,
+                                double* lp, double* grad, void* stream_);
+const char* fsmc_logreg_tc_last_error(void);
+
 /* Cross-chain diagnostic partials for effective_sample_size / R-hat
  * (analysis.py:336-418).  samples [n][m][dim]; uses rows burn..n-1.
  *   chain_mean [m][dim] (computed when lag0 == 0), acov [32][dim] = sum over chains of

@@ -113,6 +113,10 @@ def lib():
                                    ctypes.c_int32, ctypes.c_int32, _P]
     L.fsmc_logreg_epilogue.restype = S
     L.fsmc_logreg_epilogue.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]
+    L.fsmc_logreg_tc_eval.restype = S
+    L.fsmc_logreg_tc_eval.argtypes = [_P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64,
+                                      ctypes.c_int64, _P, _P, _P]
+    L.fsmc_logreg_tc_last_error.restype = ctypes.c_char_p
     L.fsmc_diag_partials.restype = S
     L.fsmc_diag_partials.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]

@@ -13,10 +13,13 @@ Bayesian logistic regression (``targets.logistic_regression_target``):
     G = (y − σ(Z)) X − Θ           [k, d]
 
 ``precision="fp64"`` evaluates in IEEE double (parity with the per-chain
-plugin up to reduction order).  ``"tf32"`` runs both contractions on the
-tensor cores (fp32 accumulation) and the σ / softplus / row-sum epilogue in
-one pass over Z (``fsmc_logreg_epilogue``); distributional parity only.
-Chains are processed in tiles so Z never exceeds ``tile`` rows.
+plugin up to reduction order).  ``"tf32"`` runs both contractions as cuBLAS
+TF32 GEMMs with the σ / softplus / row-sum epilogue in one pass over Z
+(``fsmc_logreg_epilogue``).  ``"bf16-tc"`` is the fused hand-written tcgen05
+kernel (``csrc/logreg_tc.cu``, d = 256): bf16 operands by TMA, both products
+accumulated in TMEM, the logits never stored.  The reduced precisions give
+distributional parity only.  Chains are processed in tiles so a
+materialised Z never exceeds ``tile`` rows.
 """
 
 from __future__ import annotations
@@ -30,21 +33,32 @@ __all__ = ["LogisticRegressionEvaluator"]
 
 class LogisticRegressionEvaluator:
     def __init__(self, X, y, precision: str = "fp64", tile: int = 4096):
-        if precision not in ("fp64", "tf32"):
-            raise ValueError("precision must be fp64 or tf32")
+        if precision not in ("fp64", "tf32", "bf16-tc"):
+            raise ValueError("precision must be fp64, tf32 or bf16-tc")
         self.precision = precision
         self.tile = int(tile)
         X = torch.as_tensor(X, dtype=torch.float64, device="cuda").contiguous()
         y = torch.as_tensor(y, dtype=torch.float64, device="cuda").contiguous()
         if precision == "fp64":
             self.X, self.y = X, y
-        else:
+        elif precision == "tf32":
             self.X, self.y = X.to(torch.float32), y.to(torch.float32)
             self.XT = self.X.T.contiguous()
+        else:
+            n, d = X.shape
+            if d != 256 or n % 8:
+                raise ValueError("the fused kernel needs d = 256 and n_obs a multiple of 8")
+            self.n_obs, self.d = n, d
+            self.Xb = X.to(torch.bfloat16).contiguous()
+            self.XTb = self.Xb.T.contiguous()
+            self.y = y.to(torch.float32)
+            self.theta_b = torch.empty(0, dtype=torch.bfloat16, device="cuda")
 
     def __call__(self, theta: torch.Tensor, lp: torch.Tensor, grad: torch.Tensor | None):
         if self.precision == "fp64":
             return self._fp64(theta, lp, grad)
+        if self.precision == "bf16-tc":
+            return self._fused(theta, lp, grad)
         k = theta.shape[0]
         prev = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = True
@@ -72,3 +86,18 @@ class LogisticRegressionEvaluator:
             lp[lo:hi] = (self.y * z - sp).sum(dim=1) - 0.5 * (th * th).sum(dim=1)
             if grad is not None:
                 grad[lo:hi] = (self.y - torch.sigmoid(z)) @ self.X - th
+
+    def _fused(self, theta, lp, grad):
+        k = theta.shape[0]
+        need = -(-k // 128) * 128 * self.d
+        if self.theta_b.numel() < need:
+            self.theta_b = torch.empty(need, dtype=torch.bfloat16, device="cuda")
+        g = grad if grad is not None else torch.empty((k, self.d), dtype=torch.float64, device="cuda")
+        th = theta.contiguous()
+        st = _lib.lib().fsmc_logreg_tc_eval(th.data_ptr(), k, self.theta_b.data_ptr(),
+                                            self.Xb.data_ptr(), self.XTb.data_ptr(),
+                                            self.y.data_ptr(), self.n_obs, self.d, lp.data_ptr(),
+                                            g.data_ptr(), _lib.stream_ptr())
+        if st != 0:
+            raise RuntimeError("fsmc_logreg_tc_eval: " +
+                               _lib.lib().fsmc_logreg_tc_last_error().decode())
