@@ -46,7 +46,7 @@ CONFIGS = {
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; batched TF32 gradient evaluation across chains",
                family="nuts", m=131072, n=2, d=256, variant="bundled", m_cpu=16, n_obs=100_000,
-               batched="tf32"),
+               batched="bf16-tc"),
 }
 
 
@@ -329,13 +329,16 @@ def main():
         # dominant work: the two contractions per evaluation, 4 N d flops each
         flops = 4.0 * cfg["n_obs"] * d * evals
         ach = flops / (kms / 1e3) / 1e12
-        pk = peaks.get("bf16_tflops_sustained", 1395.2) / 2.0   # dense TF32 = half of bf16
+        bf16 = cfg["batched"] == "bf16-tc"
+        pk = peaks.get("bf16_tflops_sustained", 1395.2) * (1.0 if bf16 else 0.5)
         roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
-                "frac": ach / pk, "traffic": None, "kernel": "batched logistic-regression "
-                "evaluation (cuBLAS TF32 GEMMs, interim) + fsm_advance_kernel<Nuts,128,2>",
+                "frac": ach / pk, "traffic": None,
+                "kernel": ("logreg_tc_kernel (fused tcgen05: S=Theta X^T, G+=R X in TMEM)"
+                           if bf16 else "cuBLAS TF32 GEMMs + fsmc_logreg_epilogue") +
+                          " + fsm_advance_kernel<Nuts,128,2>",
                 "kernel_ms": kms, "algorithmic_flops": flops,
-                "note": "peak = half the measured sustained bf16 figure (dense TF32 rate); "
-                        "whole run (advance + evaluation) timed"}
+                "note": "peak = measured sustained dense bf16 (half of it for TF32); whole run "
+                        "(advance rounds + evaluations) timed"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu, _ = cpu_baseline(cfg, steps=1, warmup=0)

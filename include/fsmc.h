@@ -193,12 +193,13 @@ fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, i
  * (BASELINE config 5; d must be 256):  per 128-chain tile, S = Theta X^T and
  * G += (y - sigmoid(S)) X accumulate in TMEM (bf16 operands via TMA, fp32
  * accumulation), the logits never reach HBM.  theta [k][256] fp64 in,
- * lp [k] = sum_i y z - log(1+e^z) - theta.theta/2, grad [k][256] = G - theta.
- * Scratch theta_bf16 holds ceil(k/128)*128 x 256 bf16; x_bf16 [n_obs][256]
- * and xt_bf16 [256][n_obs] are the design matrix and its transpose in bf16
- * (n_obs a multiple of 8). */
+ * lp [k] = theta.c - sum_i log(1+e^z_i) - theta.theta/2 and grad [k][256] =
+ * c - sigmoid(Z) X - theta, with c = X^T y [256] (fp64, precomputed: the
+ * label terms are linear in theta).  Scratch theta_bf16 holds
+ * ceil(k/128)*128 x 256 bf16; x_bf16 [n_obs][256] and xt_bf16 [256][n_obs]
+ * are the design matrix and its transpose in bf16 (n_obs a multiple of 8). */
 fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16, const void* x_bf16,
-                                const void* xt_bf16, const float* y, int64_t n_obs, int64_t dim,
+                                const void* xt_bf16, const double* xty, int64_t n_obs, int64_t dim,
                                 double* lp, double* grad, void* stream_);
 const char* fsmc_logreg_tc_last_error(void);
 

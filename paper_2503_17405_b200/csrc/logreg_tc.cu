@@ -4,14 +4,22 @@
 // For a tile of 128 chains (rows of Theta, bf16) the CTA streams the design
 // matrix in 64-row tiles and, per tile,
 //   S   = Theta X_tile^T          tcgen05.mma M=128 N=64  K=256  -> TMEM (fp32)
-//   R   = y - sigmoid(S),  lp += y S - softplus(S)   (epilogue warps, registers)
+//   R   = sigmoid(S),  sp += softplus(S)        (epilogue warps, registers)
 //   G  += R X_tile                tcgen05.mma M=128 N=256 K=64   -> TMEM (fp32)
 // so the [chains x N] logits never leave the SM (the flash-attention shape).
+// The label terms are linear in theta and precomputed once: with c = X^T y,
+//   lp = theta.c - sum softplus(z) - theta.theta/2,   grad = c - G - theta.
 // Operands arrive by TMA in the canonical K-major SWIZZLE_128B layout: X
 // [N][256] for the first product, X^T [256][N] for the second.  Warp roles:
-//   warp 0  TMA producer (one elected lane), double-buffered X / X^T tiles
+//   warp 0  TMA producer of Theta and the X tiles (one elected lane)
+//   warp 10 TMA producer of the X^T tiles (one elected lane)
 //   warp 1  TMEM allocator + MMA issuer (one elected lane)
-//   warps 2-5  epilogue: TMEM lane quadrant (warp % 4), one chain per thread
+// X and X^T stages have separate full/empty barriers: an X stage is released
+// as soon as the first product has read it, so X loads run ahead of the
+// epilogue while X^T (needed two tiles later) streams in behind it.
+//   warps 2-9  epilogue: TMEM lane quadrant (warp % 4) x column half, one chain
+//              row per thread; sigmoid/softplus on MUFU ex2 + rcp and an FMA
+//              polynomial for log1p
 // S is double-buffered in TMEM so the epilogue of tile i overlaps MMA1 of i+1.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -28,7 +36,8 @@ namespace {
 constexpr int BM = 128;       // chains per CTA (MMA M, TMEM lanes)
 constexpr int BN = 64;        // design rows per tile (MMA1 N, MMA2 K)
 constexpr int DF = 256;       // features (MMA1 K, MMA2 N)
-constexpr int NTHREADS = 192;
+constexpr int NTHREADS = 352;
+constexpr int N_EPI = 256;   // epilogue threads (8 warps)
 
 // shared memory map (bytes from a 1024-aligned base)
 constexpr uint32_t OFF_THETA = 0;                       // 4 atoms x [128 x 64] bf16 = 64 KB
@@ -38,8 +47,8 @@ constexpr uint32_t OFF_R = 192 * 1024;                  // 2 x [128 x 64] = 2 x 
 constexpr uint32_t OFF_BAR = 224 * 1024;                // mbarriers + TMEM address
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;   // + alignment slack
 
-enum { B_FULL0 = 0, B_EMPTY0 = 2, B_SFULL0 = 4, B_SEMPTY0 = 6, B_RFULL0 = 8, B_REMPTY0 = 10,
-       B_THETA = 12, B_GFULL = 13, N_BARS = 14 };
+enum { B_FULLX0 = 0, B_EMPTYX0 = 2, B_SFULL0 = 4, B_SEMPTY0 = 6, B_RFULL0 = 8, B_REMPTY0 = 10,
+       B_THETA = 12, B_GFULL = 13, B_FULLT0 = 14, B_EMPTYT0 = 16, N_BARS = 18 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -120,7 +129,7 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     logreg_tc_kernel(const __grid_constant__ CUtensorMap map_theta, const __grid_constant__ CUtensorMap map_x,
-                     const __grid_constant__ CUtensorMap map_xt, const float* __restrict__ y,
+                     const __grid_constant__ CUtensorMap map_xt, const double* __restrict__ xty,
                      const double* __restrict__ theta64, long long M, long long N, double* __restrict__ lp,
                      double* __restrict__ grad) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -136,11 +145,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; s++) {
-      mbar_init(bar(B_FULL0 + s), 1);
-      mbar_init(bar(B_EMPTY0 + s), 1);
+      mbar_init(bar(B_FULLX0 + s), 1);
+      mbar_init(bar(B_EMPTYX0 + s), 1);
+      mbar_init(bar(B_FULLT0 + s), 1);
+      mbar_init(bar(B_EMPTYT0 + s), 1);
       mbar_init(bar(B_SFULL0 + s), 1);
-      mbar_init(bar(B_SEMPTY0 + s), 128);
-      mbar_init(bar(B_RFULL0 + s), 128);
+      mbar_init(bar(B_SEMPTY0 + s), N_EPI);
+      mbar_init(bar(B_RFULL0 + s), N_EPI);
       mbar_init(bar(B_REMPTY0 + s), 1);
     }
     mbar_init(bar(B_THETA), 1);
@@ -159,16 +170,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tG = tmem + 128;
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------ TMA producer
+    if (lane == 0) {  // ---------------------------------- TMA producer: Theta, X
       mbar_expect_tx(bar(B_THETA), BM * DF * 2);
       for (int a = 0; a < 4; a++) tma_load_2d(sbase + OFF_THETA + a * 16384, &map_theta, bar(B_THETA), a * 64, (int)m0);
       for (int i = 0; i < T; i++) {
         const int s = i & 1;
-        mbar_wait(bar(B_EMPTY0 + s), ((i >> 1) & 1) ^ 1);
-        mbar_expect_tx(bar(B_FULL0 + s), BN * DF * 2 * 2);
+        mbar_wait(bar(B_EMPTYX0 + s), ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(bar(B_FULLX0 + s), BN * DF * 2);
         for (int a = 0; a < 4; a++)
-          tma_load_2d(sbase + OFF_X + s * 32768 + a * 8192, &map_x, bar(B_FULL0 + s), a * 64, i * BN);
-        tma_load_2d(sbase + OFF_XT + s * 32768, &map_xt, bar(B_FULL0 + s), i * BN, 0);
+          tma_load_2d(sbase + OFF_X + s * 32768 + a * 8192, &map_x, bar(B_FULLX0 + s), a * 64, i * BN);
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // ------------------------------------- TMA producer: X^T
+      for (int i = 0; i < T; i++) {
+        const int s = i & 1;
+        mbar_wait(bar(B_EMPTYT0 + s), ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(bar(B_FULLT0 + s), BN * DF * 2);
+        tma_load_2d(sbase + OFF_XT + s * 32768, &map_xt, bar(B_FULLT0 + s), i * BN, 0);
       }
     }
   } else if (warp == 1) {
@@ -180,17 +199,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       auto mma2 = [&](int i) {  // G += R_i X_i  (K = 64 rows of tile i)
         const int s = i & 1;
         mbar_wait(bar(B_RFULL0 + s), (i >> 1) & 1);
+        mbar_wait(bar(B_FULLT0 + s), (i >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 4; k++)
           mma_bf16(tG, sdesc(sbase + OFF_R + s * 16384 + k * 32), sdesc(sbase + OFF_XT + s * 32768 + k * 32), ID2,
                    (i > 0 || k > 0) ? 1u : 0u);
         mma_commit(bar(B_REMPTY0 + s));
-        mma_commit(bar(B_EMPTY0 + s));
+        mma_commit(bar(B_EMPTYT0 + s));
       };
       for (int i = 0; i < T; i++) {
         const int s = i & 1;
-        mbar_wait(bar(B_FULL0 + s), (i >> 1) & 1);
+        mbar_wait(bar(B_FULLX0 + s), (i >> 1) & 1);
         mbar_wait(bar(B_SEMPTY0 + s), ((i >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
@@ -200,13 +220,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                    sdesc(sbase + OFF_X + s * 32768 + a * 8192 + kk * 32), ID1, k > 0 ? 1u : 0u);
         }
         mma_commit(bar(B_SFULL0 + s));
+        mma_commit(bar(B_EMPTYX0 + s));
         if (i > 0) mma2(i - 1);
       }
       mma2(T - 1);
       mma_commit(bar(B_GFULL));
     }
-  } else {  // ------------------------------------------------------ epilogue
+  } else if (warp >= 2 && warp < 10) {  // ----------------------------- epilogue
     const int quad = warp & 3;            // TMEM lanes 32*quad .. 32*quad+31
+    const int half = (warp - 2) >> 2;     // columns 32*half .. 32*half+31 of each S tile
     const int row = quad * 32 + lane;     // chain within the tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     double lp_acc = 0.0;
@@ -214,53 +236,64 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int s = i & 1;
       mbar_wait(bar(B_SFULL0 + s), (i >> 1) & 1);
       tc_fence_after();
-      float z[64];
-#pragma unroll
-      for (int c = 0; c < 4; c++) tmem_ld16(tS[s] + lane_off + c * 16, z + c * 16);
+      float z[32];
+      tmem_ld16(tS[s] + lane_off + half * 32, z);
+      tmem_ld16(tS[s] + lane_off + half * 32 + 16, z + 16);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar(B_SEMPTY0 + s));
-      // R row for this chain: y - sigmoid(z); lp += y z - log(1 + e^z)
-      uint32_t packed[32];
-      const long long r0 = (long long)i * BN;
+      // R = sigmoid(z);  sp += log(1 + e^z) = max(z, 0) + log1p(e^-|z|)
+      uint32_t packed[16];
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const long long r0 = (long long)i * BN + half * 32;
+      const int valid = r0 + 32 <= N ? 32 : (int)(N > r0 ? N - r0 : 0);  // last tile only
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
+      for (int c = 0; c < 32; c += 2) {
         float rv[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-          const long long rr = r0 + c + h;
-          float r = 0.0f;
-          if (rr < N) {
-            const float zz = z[c + h];
-            const float yy = __ldg(&y[rr]);
-            const float e = __expf(-fabsf(zz));
-            const float sp = fmaxf(zz, 0.0f) + log1pf(e);
-            lp_acc += (double)(yy * zz - sp);
-            const float sg = zz >= 0.0f ? __fdividef(1.0f, 1.0f + e) : __fdividef(e, 1.0f + e);
-            r = yy - sg;
-          }
-          rv[h] = r;
+          const float zz = z[c + h];
+          float e;
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * fabsf(zz)));
+          // log1p(e) for e in (0, 1]: degree-8 fit (abs err < 4e-8)
+          float l = fmaf(e, -0.0064535442f, 0.0360884937f);
+          l = fmaf(e, l, -0.0953293897f);
+          l = fmaf(e, l, 0.1676540711f);
+          l = fmaf(e, l, -0.2407338084f);
+          l = fmaf(e, l, 0.3317990258f);
+          l = fmaf(e, l, -0.4998741238f);
+          l = fmaf(e, l, 0.9999964239f);
+          float inv;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(1.0f + e));
+          const float sp = fmaf(e, l, fmaxf(zz, 0.0f));
+          const bool ok = (c + h) < valid;
+          acc[(c + h) & 3] += ok ? sp : 0.0f;
+          rv[h] = zz >= 0.0f ? inv : e * inv;   // rows past N have x = 0: no G term
         }
         __nv_bfloat162 b2 = __floats2bfloat162_rn(rv[0], rv[1]);
         packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
       }
+      lp_acc += (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
       mbar_wait(bar(B_REMPTY0 + s), ((i >> 1) & 1) ^ 1);
       uint8_t* rbase = smem + OFF_R + s * 16384 + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll
-      for (int ch = 0; ch < 8; ch++) {  // 16-B chunk ch of this 128-B row, SWIZZLE_128B
-        uint4 v = make_uint4(packed[ch * 4], packed[ch * 4 + 1], packed[ch * 4 + 2], packed[ch * 4 + 3]);
+      for (int q = 0; q < 4; q++) {  // this warp's 16-B chunks of the 128-B row, SWIZZLE_128B
+        const int ch = half * 4 + q;
+        uint4 v = make_uint4(packed[q * 4], packed[q * 4 + 1], packed[q * 4 + 2], packed[q * 4 + 3]);
         *reinterpret_cast<uint4*>(rbase + ((ch ^ (row & 7)) << 4)) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(bar(B_RFULL0 + s));
     }
-    // G = R X summed over every tile; grad = G - theta, lp -= theta.theta / 2
+    // G = sigmoid(S) X summed over every tile:
+    //   grad = c - G - theta,  lp = theta.c - sum softplus - theta.theta / 2
+    double* lp_x = reinterpret_cast<double*>(smem + OFF_R);   // R buffers are free now
     mbar_wait(bar(B_GFULL), 0);
     tc_fence_after();
     const long long chain = m0 + row;
-    double tt = 0.0;
+    double part = -lp_acc;
 #pragma unroll 1
-    for (int c = 0; c < DF; c += 16) {
+    for (int c = half * 128; c < half * 128 + 128; c += 16) {
       float g[16];
       tmem_ld16(tG + lane_off + c, g);
       tmem_wait_ld();
@@ -268,12 +301,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int q = 0; q < 16; q++) {
           const double th = theta64[chain * DF + c + q];
-          tt += th * th;
-          grad[chain * DF + c + q] = (double)g[q] - th;
+          const double cy = __ldg(&xty[c + q]);
+          part += th * cy - 0.5 * (th * th);
+          grad[chain * DF + c + q] = (cy - (double)g[q]) - th;
         }
       }
     }
-    if (chain < M) lp[chain] = lp_acc - 0.5 * tt;
+    if (half == 1) lp_x[row] = part;
+    asm volatile("bar.sync 1, %0;" ::"n"(N_EPI));
+    if (half == 0 && chain < M) lp[chain] = part + lp_x[row];
   }
   tc_fence_before();
   __syncthreads();
@@ -331,10 +367,10 @@ const char* fsmc_logreg_tc_last_error(void) { return g_err.c_str(); }
 
 /* Fused tcgen05 logistic-regression evaluation (see fsmc.h). */
 fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16, const void* x_bf16,
-                                const void* xt_bf16, const float* y, int64_t n_obs, int64_t dim, double* lp,
+                                const void* xt_bf16, const double* xty, int64_t n_obs, int64_t dim, double* lp,
                                 double* grad, void* stream_) {
   if (dim != DF) { g_err = "fused logistic-regression kernel is compiled for d = 256"; return FSMC_ERR_UNSUPPORTED; }
-  if (!theta || !theta_bf16 || !x_bf16 || !xt_bf16 || !y || !lp || !grad || k < 0 || n_obs < 1) {
+  if (!theta || !theta_bf16 || !x_bf16 || !xt_bf16 || !xty || !lp || !grad || k < 0 || n_obs < 1) {
     g_err = "bad arguments";
     return FSMC_ERR_ARG;
   }
@@ -353,7 +389,8 @@ fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16
     cudaFuncSetAttribute(logreg_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
-  logreg_tc_kernel<<<(unsigned)(kpad / BM), NTHREADS, SMEM_BYTES, s>>>(mt, mx, mxt, y, theta, k, n_obs, lp, grad);
+  logreg_tc_kernel<<<(unsigned)(kpad / BM), NTHREADS, SMEM_BYTES, s>>>(mt, mx, mxt, xty, theta, k, n_obs, lp,
+                                                                      grad);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return FSMC_ERR_CUDA; }
   return FSMC_OK;

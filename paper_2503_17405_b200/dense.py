@@ -51,7 +51,7 @@ class LogisticRegressionEvaluator:
             self.n_obs, self.d = n, d
             self.Xb = X.to(torch.bfloat16).contiguous()
             self.XTb = self.Xb.T.contiguous()
-            self.y = y.to(torch.float32)
+            self.xty = (X.T @ y).contiguous()     # label terms, linear in theta (fp64)
             self.theta_b = torch.empty(0, dtype=torch.bfloat16, device="cuda")
 
     def __call__(self, theta: torch.Tensor, lp: torch.Tensor, grad: torch.Tensor | None):
@@ -96,7 +96,7 @@ class LogisticRegressionEvaluator:
         th = theta.contiguous()
         st = _lib.lib().fsmc_logreg_tc_eval(th.data_ptr(), k, self.theta_b.data_ptr(),
                                             self.Xb.data_ptr(), self.XTb.data_ptr(),
-                                            self.y.data_ptr(), self.n_obs, self.d, lp.data_ptr(),
+                                            self.xty.data_ptr(), self.n_obs, self.d, lp.data_ptr(),
                                             g.data_ptr(), _lib.stream_ptr())
         if st != 0:
             raise RuntimeError("fsmc_logreg_tc_eval: " +
