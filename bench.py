@@ -45,7 +45,7 @@ CONFIGS = {
                family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4),
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; batched TF32 gradient evaluation across chains",
-               family="nuts", m=131072, n=2, d=256, variant="bundled", m_cpu=16, n_obs=100_000,
+               family="nuts", m=131072, n=8, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
                batched="bf16-tc"),
 }
 
@@ -136,7 +136,7 @@ def cpu_baseline(cfg, steps=1, warmup=0, seed=0):
     from oracle import oracle as O
     kern, targ = make_workload(cfg, oracle=True)
     threads = os.cpu_count() or 1
-    m_cpu, n = cfg["m_cpu"], cfg["n"]
+    m_cpu, n = cfg["m_cpu"], cfg.get("n_cpu", cfg["n"])
     times = []
     for s in range(warmup + steps):
         t0 = time.perf_counter()

@@ -12,14 +12,14 @@
 // Operands arrive by TMA in the canonical K-major SWIZZLE_128B layout: X
 // [N][256] for the first product, X^T [256][N] for the second.  Warp roles:
 //   warp 0  TMA producer of Theta and the X tiles (one elected lane)
-//   warp 10 TMA producer of the X^T tiles (one elected lane)
+//   warp W_XT  TMA producer of the X^T tiles (one elected lane)
 //   warp 1  TMEM allocator + MMA issuer (one elected lane)
 // X and X^T stages have separate full/empty barriers: an X stage is released
 // as soon as the first product has read it, so X loads run ahead of the
 // epilogue while X^T (needed two tiles later) streams in behind it.
-//   warps 2-9  epilogue: TMEM lane quadrant (warp % 4) x column half, one chain
-//              row per thread; sigmoid/softplus on MUFU ex2 + rcp and an FMA
-//              polynomial for log1p
+//   warps 2 .. 2+4*EPI_SPLIT-1  epilogue: TMEM lane quadrant (warp % 4) x a
+//              column slice, one chain row per thread; sigmoid / softplus on
+//              MUFU ex2, rcp and lg2
 // S is double-buffered in TMEM so the epilogue of tile i overlaps MMA1 of i+1.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -36,8 +36,11 @@ namespace {
 constexpr int BM = 128;       // chains per CTA (MMA M, TMEM lanes)
 constexpr int BN = 64;        // design rows per tile (MMA1 N, MMA2 K)
 constexpr int DF = 256;       // features (MMA1 K, MMA2 N)
-constexpr int NTHREADS = 352;
-constexpr int N_EPI = 256;   // epilogue threads (8 warps)
+constexpr int EPI_SPLIT = 2;                 // epilogue warps per TMEM lane quadrant
+constexpr int N_EPI = 128 * EPI_SPLIT;        // epilogue threads
+constexpr int COLS = BN / EPI_SPLIT;          // S columns per epilogue thread
+constexpr int W_XT = 2 + N_EPI / 32;          // warp index of the X^T producer
+constexpr int NTHREADS = 32 * (W_XT + 1);
 
 // shared memory map (bytes from a 1024-aligned base)
 constexpr uint32_t OFF_THETA = 0;                       // 4 atoms x [128 x 64] bf16 = 64 KB
@@ -62,15 +65,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier
+// unit instead of re-issuing its poll loop (which would steal issue slots
+// from the epilogue warps sharing its scheduler)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0,
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tma_load_2d(sbase + OFF_X + s * 32768 + a * 8192, &map_x, bar(B_FULLX0 + s), a * 64, i * BN);
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == W_XT) {
     if (lane == 0) {  // ------------------------------------- TMA producer: X^T
       for (int i = 0; i < T; i++) {
         const int s = i & 1;
@@ -226,9 +232,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mma2(T - 1);
       mma_commit(bar(B_GFULL));
     }
-  } else if (warp >= 2 && warp < 10) {  // ----------------------------- epilogue
+  } else if (warp >= 2 && warp < W_XT) {  // ---------------------------- epilogue
     const int quad = warp & 3;            // TMEM lanes 32*quad .. 32*quad+31
-    const int half = (warp - 2) >> 2;     // columns 32*half .. 32*half+31 of each S tile
+    const int half = (warp - 2) >> 2;     // columns COLS*half .. COLS*half+COLS-1 of each S tile
     const int row = quad * 32 + lane;     // chain within the tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     double lp_acc = 0.0;
@@ -236,36 +242,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int s = i & 1;
       mbar_wait(bar(B_SFULL0 + s), (i >> 1) & 1);
       tc_fence_after();
-      float z[32];
-      tmem_ld16(tS[s] + lane_off + half * 32, z);
-      tmem_ld16(tS[s] + lane_off + half * 32 + 16, z + 16);
+      float z[COLS];
+#pragma unroll
+      for (int q = 0; q < COLS; q += 16) tmem_ld16(tS[s] + lane_off + half * COLS + q, z + q);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar(B_SEMPTY0 + s));
       // R = sigmoid(z);  sp += log(1 + e^z) = max(z, 0) + log1p(e^-|z|)
-      uint32_t packed[16];
+      uint32_t packed[COLS / 2];
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      const long long r0 = (long long)i * BN + half * 32;
-      const int valid = r0 + 32 <= N ? 32 : (int)(N > r0 ? N - r0 : 0);  // last tile only
+      const long long r0 = (long long)i * BN + half * COLS;
+      const int valid = r0 + COLS <= N ? COLS : (int)(N > r0 ? N - r0 : 0);  // last tile only
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
+      for (int c = 0; c < COLS; c += 2) {
         float rv[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const float zz = z[c + h];
           float e;
           asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * fabsf(zz)));
-          // log1p(e) for e in (0, 1]: degree-8 fit (abs err < 4e-8)
-          float l = fmaf(e, -0.0064535442f, 0.0360884937f);
-          l = fmaf(e, l, -0.0953293897f);
-          l = fmaf(e, l, 0.1676540711f);
-          l = fmaf(e, l, -0.2407338084f);
-          l = fmaf(e, l, 0.3317990258f);
-          l = fmaf(e, l, -0.4998741238f);
-          l = fmaf(e, l, 0.9999964239f);
-          float inv;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(1.0f + e));
-          const float sp = fmaf(e, l, fmaxf(zz, 0.0f));
+          const float ope = 1.0f + e;
+          float inv, l2;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(ope));
+          asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(ope));   // log1p(e) = ln2 log2(1+e)
+          const float sp = fmaf(0.6931471805599453f, l2, fmaxf(zz, 0.0f));
           const bool ok = (c + h) < valid;
           acc[(c + h) & 3] += ok ? sp : 0.0f;
           rv[h] = zz >= 0.0f ? inv : e * inv;   // rows past N have x = 0: no G term
@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(bar(B_REMPTY0 + s), ((i >> 1) & 1) ^ 1);
       uint8_t* rbase = smem + OFF_R + s * 16384 + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll
-      for (int q = 0; q < 4; q++) {  // this warp's 16-B chunks of the 128-B row, SWIZZLE_128B
-        const int ch = half * 4 + q;
+      for (int q = 0; q < COLS / 8; q++) {  // this warp's 16-B chunks of the 128-B row, SWIZZLE_128B
+        const int ch = half * (COLS / 8) + q;
         uint4 v = make_uint4(packed[q * 4], packed[q * 4 + 1], packed[q * 4 + 2], packed[q * 4 + 3]);
         *reinterpret_cast<uint4*>(rbase + ((ch ^ (row & 7)) << 4)) = v;
       }
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const long long chain = m0 + row;
     double part = -lp_acc;
 #pragma unroll 1
-    for (int c = half * 128; c < half * 128 + 128; c += 16) {
+    for (int c = half * (DF / EPI_SPLIT); c < (half + 1) * (DF / EPI_SPLIT); c += 16) {
       float g[16];
       tmem_ld16(tG + lane_off + c, g);
       tmem_wait_ld();
@@ -307,9 +307,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     }
-    if (half == 1) lp_x[row] = part;
+    if (half > 0) lp_x[(half - 1) * BM + row] = part;
     asm volatile("bar.sync 1, %0;" ::"n"(N_EPI));
-    if (half == 0 && chain < M) lp[chain] = part + lp_x[row];
+    if (half == 0 && chain < M) {
+#pragma unroll
+      for (int h = 1; h < EPI_SPLIT; h++) part += lp_x[(h - 1) * BM + row];
+      lp[chain] = part;
+    }
   }
   tc_fence_before();
   __syncthreads();
