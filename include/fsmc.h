@@ -62,7 +62,7 @@ typedef struct fsmc_kernel {
   double proposal_scale;        /* drmh: proposal N(y, scale^2 I) */
   double step_size;             /* nuts: epsilon */
   int32_t max_depth;            /* nuts */
-  int32_t split_body;           /* reserved (drmh split body), must be 0 */
+  int32_t split_body;           /* drmh: 1 = 4-way split proposal (drmh.py:106-156), 6 states */
   double divergence_threshold;  /* nuts */
 } fsmc_kernel;
 
@@ -113,8 +113,8 @@ typedef struct fsmc_outputs {
 enum {
   FSMC_I_COUNTER = 0, FSMC_I_STREAM = 1, FSMC_I_STATE = 2, FSMC_I_TICK = 3, FSMC_I_COUNT = 4,
   FSMC_I_ERR_KIND = 5, FSMC_I_ERR_LABEL = 6, FSMC_I_ERR_TICK = 7, FSMC_I_ERR_ITER = 8,
-  FSMC_I_SHARED = 9, FSMC_I_BLOCKS = 10 /* 6 slots */, FSMC_I_PEND = 16 /* 3 slots */,
-  FSMC_I_FAMILY = 19 /* family-private slots 19..30 */,
+  FSMC_I_SHARED = 9, FSMC_I_BLOCKS = 10 /* 6 slots */, FSMC_I_PEND = 16 /* 4 slots */,
+  FSMC_I_FAMILY = 20 /* family-private slots 20..30 */,
   FSMC_I_RESUME = 31 /* batched mode: suspended-at-evaluation record */
 };
 /* error kinds in FSMC_I_ERR_KIND */

@@ -4,6 +4,7 @@
 // kernels and ptxas time grows with the unrolled register footprint.
 #pragma once
 #define FSMC_DRMH_CONFIGS(X) X(1, 1) X(1, 2) X(1, 4) X(1, 10) X(1, 16) X(2, 5) X(4, 3) X(32, 4)
+#define FSMC_DRMH_SPLIT_CONFIGS(X) X(1, 1) X(1, 2) X(1, 4) X(1, 10) X(32, 4)
 #define FSMC_ESS_CONFIGS(X) X(1, 2) X(1, 4) X(32, 1) X(32, 2) X(32, 4) X(32, 8) X(128, 8)
 #define FSMC_NUTS_CONFIGS(X) X(1, 2) X(2, 2) X(4, 3) X(4, 4) X(8, 2) X(32, 1) X(32, 4) X(128, 2)
 

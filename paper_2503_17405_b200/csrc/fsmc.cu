@@ -265,7 +265,10 @@ fsmc_status fsmc_state_layout(const fsmc_kernel* k, int64_t dim, int32_t* n_vec,
                               int32_t* n_loop, int32_t* n_states) {
   if (!k) return fail(FSMC_ERR_ARG, "null kernel");
   switch (k->family) {
-    case FSMC_DRMH: *n_vec = 2; *n_scal = 3; *n_loop = 1; *n_states = 3; break;
+    case FSMC_DRMH:
+      if (k->split_body) { *n_vec = 3; *n_scal = 4; *n_loop = 4; *n_states = 6; }
+      else { *n_vec = 2; *n_scal = 3; *n_loop = 1; *n_states = 3; }
+      break;
     case FSMC_ESS: *n_vec = 3; *n_scal = 6; *n_loop = 1; *n_states = 3; break;
     case FSMC_NUTS:
       *n_vec = 12 + 2 * k->max_depth; *n_scal = 3; *n_loop = 3; *n_states = 5;
@@ -319,7 +322,7 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
   p.tick_limit = tick_limit;
   p.variant = variant;
   p.mode = mode;
-  int K = k->family == FSMC_NUTS ? 5 : 3;
+  int K = k->family == FSMC_NUTS ? 5 : (k->family == FSMC_DRMH && k->split_body ? 6 : 3);
   for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
   cudaStream_t cs = (cudaStream_t)stream_;
   p.next_chain = scratch().words;
@@ -348,7 +351,7 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
   p.tick_limit = tick_limit;
   p.variant = variant;
   p.mode = mode;
-  int K = k->family == FSMC_NUTS ? 5 : 3;
+  int K = k->family == FSMC_NUTS ? 5 : (k->family == FSMC_DRMH && k->split_body ? 6 : 3);
   for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
   p.b_lp = lp;
   p.b_grad = grad;

@@ -233,12 +233,15 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
       } else {  // while _continue(z) / _below_threshold(z)
         bool co = live && f.loop_continue(p);
         if (grid_any(p, co, phase)) s = co ? 2 : 0;
-        else { s = 3; pc = PC_END; }
+        else { s = FF::K; pc = PC_END; }
       }
-      if (live && s) {
+      // one while-loop body: PROPOSE, or the split body's states 2..K-1
+      const int s_last = (s == 2 && FF::K == 6) ? 5 : s;
+#pragma unroll 1
+      for (int ss = s; live && s && ss <= s_last; ss++) {
         bool did = false;
-        if (!run_state<FF, G, E, TK>(p, c, f, s, did, sm, grp)) live = false;
-        count_block<FF>(c, s);
+        if (!run_state<FF, G, E, TK>(p, c, f, ss, did, sm, grp)) live = false;
+        count_block<FF>(c, ss);
         if (did) c.shared++;
       }
       if (pc == PC_END) break;

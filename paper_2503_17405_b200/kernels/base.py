@@ -34,6 +34,7 @@ class KernelBundle:
     step_size: float = 0.0
     max_depth: int = 0
     divergence_threshold: float = 1000.0
+    split_body: bool = False
 
     def __post_init__(self):
         if not set(self.iter_states) <= self.fsm.loop_states:
@@ -46,7 +47,7 @@ class KernelBundle:
         k.proposal_scale = self.proposal_scale
         k.step_size = self.step_size
         k.max_depth = self.max_depth
-        k.split_body = 0
+        k.split_body = int(self.split_body)
         k.divergence_threshold = self.divergence_threshold
         return k
 

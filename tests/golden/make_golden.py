@@ -244,6 +244,16 @@ def main():
     X, y = logreg_data(512, 16, seed=0)
     run_case("nuts_logreg512x16", nuts_kernel(0.1, 8), logreg_target(X, y),
              m=6, n=40, seed=9, variants=("plain", "bundled"), extra={"X": X, "y": y})
+    main_split_only()
+
+
+def main_split_only():
+    run_case("drmh_split_std1", drmh_kernel(50, 0.4, split_body=True),
+             gaussian_target(np.zeros(1), np.eye(1)), m=6, n=80, seed=5,
+             variants=("plain", "bundled"), tick_chunk=1)
+    run_case("drmh_split_mog10", drmh_kernel(100, 0.1, split_body=True),
+             correlated_mog_target(10, 0.9, [-3.0, 0.0, 3.0]), m=8, n=40, seed=6,
+             variants=("plain", "bundled"))
 
 
 def main_logreg_only():
@@ -255,5 +265,7 @@ def main_logreg_only():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "logreg":
         main_logreg_only()
+    elif len(sys.argv) > 1 and sys.argv[1] == "split":
+        main_split_only()
     else:
         main()

@@ -31,7 +31,12 @@ CASES = {
     "nuts_funnel5": (("plain", "bundled", "standard"), ("nuts", 0.3, 5, 50.0), ("funnel", 5)),
     "nuts_std2": (("plain", "bundled", "standard"), ("nuts", 0.9, 4, 1000.0), ("gauss", np.zeros(2), np.eye(2))),
     "nuts_logreg512x16": (("plain", "bundled", "standard"), ("nuts", 0.1, 8, 1000.0), ("logreg",)),
+    "drmh_split_std1": (("plain", "bundled", "standard"), ("drmh-split", 50, 0.4), ("gauss", np.zeros(1), np.eye(1))),
+    "drmh_split_mog10": (("plain", "bundled", "standard"), ("drmh-split", 100, 0.1), ("mog", 10, 0.9, (-3.0, 0.0, 3.0))),
 }
+
+# cases the oracle does not restate (checked against the goldens on the device only)
+DEVICE_ONLY = {"drmh_split_std1", "drmh_split_mog10"}
 
 
 def oracle_kernel(spec):
@@ -67,6 +72,8 @@ def oracle_target(spec):
 
 def device_kernel(spec):
     import paper_2503_17405_b200 as fm
+    if spec[0] == "drmh-split":
+        return fm.drmh_kernel(spec[1], spec[2], split_body=True)
     if spec[0] == "drmh":
         return fm.drmh_kernel(spec[1], spec[2])
     if spec[0] == "ess":

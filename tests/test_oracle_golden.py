@@ -8,7 +8,7 @@ import math
 import numpy as np
 import pytest
 
-from golden_cases import CASES, load, oracle_kernel, oracle_target, rel_err
+from golden_cases import CASES, DEVICE_ONLY, load, oracle_kernel, oracle_target, rel_err
 from oracle import oracle as O
 
 SAMPLE_TOL = 1e-12
@@ -38,7 +38,7 @@ def test_survey_kats():
     assert lib.or_normal(0, 0, 0) == 0.3766482861700982
 
 
-@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("name", sorted(set(CASES) - DEVICE_ONLY))
 def test_oracle_matches_reference(name):
     variants, kspec, tspec = CASES[name]
     g = load(name)
