@@ -36,8 +36,11 @@ inline size_t smem_bytes(int dim) {
 
 // registers: 4 resident blocks per SM for thread-per-chain configurations so
 // that a full batch of chains is co-resident (no second wave)
+#ifndef FSMC_WARP_MIN_BLOCKS
+#define FSMC_WARP_MIN_BLOCKS 3
+#endif
 template <int G>
-__host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : 1; }
+__host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : (G == 32 ? FSMC_WARP_MIN_BLOCKS : 1); }
 
 struct LaunchCtx {
   int num_sms;
