@@ -35,6 +35,11 @@ for r in csv.reader(io.StringIO(txt)):
     src[key] = r[1].strip()[:70]
     ie = r[hdr["Instructions Executed"]]
     if ie and ie != "-":
+        try:
+            int(ie), int(r[hdr["Thread Instructions Executed"]] or 0)
+            int(r[hdr["Warp Stall Sampling (All Samples)"]] or 0)
+        except ValueError:
+            continue   # a source line whose text broke the CSV quoting
         inst[key] += int(ie)
         tv = r[hdr["Thread Instructions Executed"]]
         thr[key] += int(tv) if tv not in ("", "-") else 0
