@@ -168,6 +168,7 @@ class ChainBatch:
         self.ints = torch.zeros((self.m, _lib.FSMC_NINT), dtype=torch.int64, device="cuda")
         self.err_key = torch.full((1,), -1, dtype=torch.int64, device="cuda")
         self.active_mask = [True] * self.m
+        self._ran = False
 
     def struct(self, lo: int = 0, hi: int | None = None) -> _lib.State:
         hi = self.m if hi is None else hi
@@ -205,6 +206,16 @@ class ChainBatch:
         row = self.ints[j].tolist()
         return RngKey(self.seed & ((1 << 64) - 1), row[_lib.I_STREAM] & ((1 << 64) - 1),
                       row[_lib.I_COUNTER] & ((1 << 64) - 1))
+
+    def host_summary(self):
+        """One device->host read: per chain (count, tick, error kind, error
+        tick, error label, error sample index, shared evaluations) and the
+        first-failure key."""
+        cols = [_lib.I_COUNT, _lib.I_TICK, _lib.I_ERR_KIND, _lib.I_ERR_TICK, _lib.I_ERR_LABEL,
+                _lib.I_ERR_ITER, _lib.I_SHARED]
+        flat = torch.cat([self.ints[:, cols].reshape(-1), self.err_key]).cpu()
+        key = int(flat[-1]) & ((1 << 64) - 1)
+        return flat[:-1].reshape(self.m, len(cols)), key
 
     def first_error(self):
         key = int(self.err_key.item()) & ((1 << 64) - 1)
@@ -286,7 +297,7 @@ def init_batch(bundle, target, m: int, seed: int, x0=None, init_jitter: float = 
 def _validate_run_args(batch: ChainBatch, n: int):
     if n < 1:
         raise ValueError(f"need n >= 1 samples, got {n}")
-    if bool((batch.ints[:, _lib.I_COUNT] != 0).any()):
+    if batch._ran:   # lockstep.py:231-235 (a batch is fresh until a driver runs it)
         raise ValueError("batch has already been run; build a fresh one")
 
 
@@ -379,34 +390,37 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     launch(0, limit)
     if _timing is not None:
         ev[1].record()
-    info = batch.ints[:, [_lib.I_COUNT, _lib.I_TICK, _lib.I_ERR_KIND, _lib.I_ERR_TICK]].cpu()
-    counts, cticks, ekind, etick = (info[:, i] for i in range(4))
-    errored = ekind != _lib.E_NONE
+    info, key = batch.host_summary()          # one device->host read
+    counts, cticks = info[:, 0], info[:, 1]
+    errored = info[:, 2] != _lib.E_NONE
     all_done = bool((counts >= n).all())
     if all_done:
-        tmax = int(cticks.max())
-        tick_count = -(-tmax // tick_chunk) * tick_chunk
+        tick_count = -(-int(cticks.max()) // tick_chunk) * tick_chunk
     else:
         tick_count = limit
-    first_err = int(etick[errored].min()) if bool(errored.any()) else _NO_LIMIT
+    first_err = int(info[errored, 3].min()) if bool(errored.any()) else _NO_LIMIT
     run_to = min(tick_count, first_err)
     if run_to < _NO_LIMIT and (surplus or first_err < _NO_LIMIT) and int(cticks.min()) < run_to:
         launch(1, run_to)
-    torch.cuda.synchronize()
+        info, key = batch.host_summary()
+    else:
+        torch.cuda.synchronize()
     walltime = time.perf_counter() - t0
     if _timing is not None:
         _timing["run_kernel_ms"] = ev[0].elapsed_time(ev[1])
     batch.active_mask = [False] * m
+    batch._ran = True
 
-    err = batch.first_error()
-    if err is not None:
-        j, kind, label, etick_j, eiter = err
+    if key != (1 << 64) - 1:
+        j = key & ((1 << 24) - 1)
+        kind, label, etick_j, eiter = (int(v) for v in info[j, 2:6])
         if etick_j <= tick_count:
             raise KernelRunError(chain=j, iteration=eiter, cause=_cause(bundle, kind, label))
-    counts_now = batch.ints[:, _lib.I_COUNT].cpu()
+    counts_now = info[:, 0]
     n_done = n if all_done else int(counts_now.min())
     ledger = _fsm_ledger(bundle, params, step_variant, batch, loops, ticks_out, n_done,
-                         tick_count if all_done else limit, walltime, output)
+                         tick_count if all_done else limit, walltime, output,
+                         native_shared=int(info[:, 6].sum()))
     if hasattr(launch, "stats"):
         ledger.extras.update(launch.stats)
     if not all_done:
@@ -462,7 +476,7 @@ def _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evalu
 
 
 def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks, walltime,
-                output) -> CostLedger:
+                output, native_shared: int) -> CostLedger:
     """lockstep.py:419-451"""
     K = bundle.fsm.n_states
     loop_states = bundle.loop_states
@@ -477,7 +491,7 @@ def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks,
         block_exec_counts=_convert(blocks, output), charged_cost=ticks * tc, walltime=walltime,
         regime=f"fsm-{variant}", tick_cost=tc,
         shared_evals_per_tick=params.shared_evals_per_tick(variant),
-        native_shared_evals=int(batch.ints[:, _lib.I_SHARED].sum()), sample_ticks=st)
+        native_shared_evals=native_shared, sample_ticks=st)
 
 
 def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
@@ -509,6 +523,7 @@ def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
     torch.cuda.synchronize()
     walltime = time.perf_counter() - t0
     batch.active_mask = [False] * m
+    batch._ran = True
     errs = batch.ints[:, [_lib.I_ERR_KIND, _lib.I_ERR_ITER]].cpu()
     bad = (errs[:, 0] != _lib.E_NONE).nonzero().flatten().tolist()
     if bad:
