@@ -261,7 +261,7 @@ def main():
         mom = analysis.diag_moments(samples, burn=burn)
         if world > 1:
             loc = distributed.LocalMoments(mom.n, analysis_chain_means(samples, burn),
-                                           mom.max_chain_var, mom.acov_tile)
+                                           mom.max_chain_var, mom.acov_tile, mom.acov_all)
             mom = distributed.allreduce_moments(loc, device=dev)
         ess = analysis.ess_from_moments(mom)
         ess_pooled = ess.pooled

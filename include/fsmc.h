@@ -207,10 +207,12 @@ const char* fsmc_logreg_tc_last_error(void);
  * (analysis.py:336-418).  samples [n][m][dim]; uses rows burn..n-1.
  *   chain_mean [m][dim] (computed when lag0 == 0), acov [32][dim] = sum over chains of
  *   the lag-(lag0+t) autocovariance (one tile of 32 lags per call;
- *   divided by the row count, analysis.py:344-347). */
+ *   divided by the row count, analysis.py:344-347), chain_var [m][dim]
+ *   (optional, lag0 == 0): each chain's population variance.  One coalesced
+ *   pass over the samples per tile. */
 fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int64_t dim,
                                int64_t burn, int64_t lag0, int64_t n_lags, double* chain_mean,
-                               double* acov, void* stream_);
+                               double* acov, double* chain_var, void* stream_);
 
 #ifdef __cplusplus
 }

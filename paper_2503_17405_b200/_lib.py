@@ -119,7 +119,7 @@ def lib():
     L.fsmc_logreg_tc_last_error.restype = ctypes.c_char_p
     L.fsmc_diag_partials.restype = S
     L.fsmc_diag_partials.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
-                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P]
     if L.fsmc_abi_version() != 1:
         raise EngineUnavailable("libfsmc.so ABI version mismatch")
     _lib = L

@@ -55,6 +55,7 @@ class DiagMoments:
     var_means: np.ndarray
     max_chain_var: np.ndarray
     acov_tile: Callable[[int], np.ndarray]
+    acov_all: Callable[[], np.ndarray] | None = None   # [n, d] sums over chains, all lags
 
 
 def _as_device(chains) -> torch.Tensor:
@@ -76,35 +77,60 @@ def diag_moments(chains, burn: int = 0) -> DiagMoments:
     n = n_all - burn
     lib = _lib.lib()
     mean = torch.empty((m, d), dtype=torch.float64, device="cuda")
+    var = torch.empty((m, d), dtype=torch.float64, device="cuda")
     tile = torch.empty((LAG_TILE, d), dtype=torch.float64, device="cuda")
     _lib.check(lib.fsmc_diag_partials(S.data_ptr(), n_all, m, d, burn, 0, LAG_TILE,
-                                      mean.data_ptr(), tile.data_ptr(), _lib.stream_ptr()),
-               "fsmc_diag_partials")
+                                      mean.data_ptr(), tile.data_ptr(), var.data_ptr(),
+                                      _lib.stream_ptr()), "fsmc_diag_partials")
     first = tile.cpu().numpy()
     var_means = mean.var(dim=0, unbiased=True).cpu().numpy() if m > 1 else np.zeros(d)
-    chain_var = S[burn:].var(dim=0, unbiased=False).amax(dim=0).cpu().numpy()
+    chain_var = var.amax(dim=0).cpu().numpy()
 
     def acov_tile(k: int) -> np.ndarray:
         if k == 0:
             return first
         _lib.check(lib.fsmc_diag_partials(S.data_ptr(), n_all, m, d, burn, k * LAG_TILE,
-                                          LAG_TILE, mean.data_ptr(), tile.data_ptr(),
+                                          LAG_TILE, mean.data_ptr(), tile.data_ptr(), None,
                                           _lib.stream_ptr()), "fsmc_diag_partials")
         return tile.cpu().numpy()
 
+    def acov_all() -> np.ndarray:
+        """Every lag at once by FFT (analysis.py:344-347), for slowly mixing
+        chains whose Geyer truncation needs many lag tiles."""
+        size = 1 << int(math.ceil(math.log2(2 * n)))
+        out = torch.zeros((n, d), dtype=torch.float64, device="cuda")
+        chunk = max(1, (1 << 28) // (size * d))   # ~4 GB of complex work at a time
+        for lo in range(0, m, chunk):
+            hi = min(m, lo + chunk)
+            c = (S[burn:, lo:hi, :] - mean[lo:hi]).permute(1, 2, 0)   # [chains, d, n]
+            f = torch.fft.rfft(c, n=size, dim=2)
+            ac = torch.fft.irfft(f * f.conj(), n=size, dim=2)[:, :, :n] / n
+            out += ac.sum(dim=0).T
+        return out.cpu().numpy()
+
     return DiagMoments(n=n, m=m, d=d, var_means=var_means, max_chain_var=chain_var,
-                       acov_tile=acov_tile)
+                       acov_tile=acov_tile, acov_all=acov_all)
 
 
 class _Acov:
-    """Lazily tiled mean (over chains) autocovariance of one dimension set."""
+    """Mean (over chains) autocovariance of one dimension set: lag tiles on
+    demand, switching to one FFT over every lag once the truncation point is
+    beyond a few tiles."""
+
+    TILE_LIMIT = 3
 
     def __init__(self, mom: DiagMoments):
         self.mom = mom
         self.tiles: list[np.ndarray] = []
+        self.full = None
 
     def __call__(self, t: int, k: int) -> float:
+        if self.full is not None:
+            return float(self.full[t, k]) if t < self.full.shape[0] else 0.0
         tile = t // LAG_TILE
+        if tile >= self.TILE_LIMIT and self.mom.acov_all is not None:
+            self.full = self.mom.acov_all() / self.mom.m
+            return self(t, k)
         while len(self.tiles) <= tile:
             self.tiles.append(self.mom.acov_tile(len(self.tiles)) / self.mom.m)
         return float(self.tiles[tile][t % LAG_TILE, k])

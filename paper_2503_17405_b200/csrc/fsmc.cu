@@ -110,32 +110,69 @@ __global__ void diag_mean_kernel(const double* S, long long n, long long m, long
 }
 
 constexpr int kLagTile = 32;
-// thread per (chain, dim): lags lag0 .. lag0+kLagTile-1 of the centred series,
-// accumulated into acov[t][k] (sum over chains).  Warps read consecutive
-// (chain, dim) addresses of one sample row, so the row loads coalesce.
-__global__ void diag_acov_kernel(const double* S, long long n, long long m, long long d, long long burn,
-                                 long long lag0, const double* mean, double* acov) {
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= m * d) return;
-  const long long k = idx % d;
+// Thread per (chain, dim) series c_i = S[burn+i][j][k] - mean: lags
+// lag0 .. lag0+31 of sum_i c_i c_{i+lag}, each series element read once.
+// The lagged stream lives in a 32-entry register ring (indices fixed at
+// compile time by unrolling the row loop 32-fold), so the kernel is one
+// coalesced pass over the samples (rows of m*d consecutive doubles).  Sums
+// over chains go through shared memory first (one global atomic per block
+// and (lag, dim)); lag 0 of tile 0 also yields each chain's variance.
+__global__ void __launch_bounds__(128) diag_acov_kernel(const double* __restrict__ S, long long n, long long m,
+                                                        long long d, long long burn, long long lag0,
+                                                        const double* __restrict__ mean, double* acov,
+                                                        double* chain_var) {
+  extern __shared__ double red[];   // [32][d] when d <= 128
+  const bool smem_red = d <= 128;
+  if (smem_red) {
+    for (int i = threadIdx.x; i < kLagTile * d; i += blockDim.x) red[i] = 0.0;
+    __syncthreads();
+  }
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool live = idx < m * d;
+  const long long k = live ? idx % d : 0;
   const long long N = n - burn;
-  const double mu = mean[idx];
   double acc[kLagTile];
 #pragma unroll
   for (int t = 0; t < kLagTile; t++) acc[t] = 0.0;
-  const size_t stride = (size_t)m * d;
-  const double* col = S + (size_t)burn * stride + idx;
-  for (long long i = 0; i + lag0 < N; i++) {
-    double ci = col[(size_t)i * stride] - mu;
+  if (live) {
+    const double mu = mean[idx];
+    const size_t stride = (size_t)m * d;
+    const double* col = S + (size_t)burn * stride + idx;
+    auto b_at = [&](long long r) -> double {   // lagged stream c_{r + lag0}, 0 past the end
+      long long rr = r + lag0;
+      return rr < N ? __ldg(&col[(size_t)rr * stride]) - mu : 0.0;
+    };
+    double ring[kLagTile];
 #pragma unroll
-    for (int t = 0; t < kLagTile; t++) {
-      long long ii = i + lag0 + t;
-      if (ii < N) acc[t] += ci * (col[(size_t)ii * stride] - mu);
+    for (int t = 0; t < kLagTile; t++) ring[t] = b_at(t);
+    const long long imax = N - lag0;   // rows with at least one partner
+    for (long long i0 = 0; i0 < imax; i0 += kLagTile) {
+#pragma unroll
+      for (int q = 0; q < kLagTile; q++) {
+        const long long i = i0 + q;
+        if (i < imax) {
+          const double a = __ldg(&col[(size_t)i * stride]) - mu;
+#pragma unroll
+          for (int t = 0; t < kLagTile; t++) acc[t] = fma(a, ring[(q + t) & (kLagTile - 1)], acc[t]);
+        }
+        ring[q] = b_at(i + kLagTile);   // slot q now holds b_{i+32}
+      }
     }
+    if (lag0 == 0 && chain_var) chain_var[idx] = acc[0] / (double)N;
   }
+  if (smem_red) {
+    if (live) {
 #pragma unroll
-  for (int t = 0; t < kLagTile; t++)
-    if (lag0 + t < N) atomicAdd(&acov[t * d + k], acc[t] / (double)N);
+      for (int t = 0; t < kLagTile; t++) atomicAdd(&red[t * d + k], acc[t] / (double)N);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kLagTile * d; i += blockDim.x)
+      if (lag0 + i / d < N) atomicAdd(&acov[i], red[i]);
+  } else if (live) {
+#pragma unroll
+    for (int t = 0; t < kLagTile; t++)
+      if (lag0 + t < N) atomicAdd(&acov[t * d + k], acc[t] / (double)N);
+  }
 }
 
 // logistic-regression epilogue: one pass over Z [rows][N] (see fsmc.h)
@@ -422,7 +459,7 @@ fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, i
 
 fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int64_t dim, int64_t burn,
                                int64_t lag0, int64_t n_lags, double* chain_mean, double* acov,
-                               void* stream_) {
+                               double* chain_var, void* stream_) {
   if (!samples || n - burn < 2 || m < 1 || dim < 1 || !chain_mean) return fail(FSMC_ERR_ARG, "bad diag args");
   cudaStream_t cs = (cudaStream_t)stream_;
   if (lag0 == 0) {
@@ -434,8 +471,9 @@ fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int6
     if (n_lags != kLagTile) return fail(FSMC_ERR_ARG, "n_lags must be 32 (one lag tile per call)");
     CUDA_TRY(cudaMemsetAsync(acov, 0, sizeof(double) * kLagTile * dim, cs));
     long long tot = m * dim;
-    diag_acov_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, cs>>>(samples, n, m, dim, burn, lag0,
-                                                                    chain_mean, acov);
+    size_t sm = dim <= 128 ? sizeof(double) * kLagTile * dim : 0;
+    diag_acov_kernel<<<(unsigned)((tot + 127) / 128), 128, sm, cs>>>(samples, n, m, dim, burn, lag0,
+                                                                     chain_mean, acov, chain_var);
     CUDA_TRY(cudaGetLastError());
   }
   return FSMC_OK;

@@ -25,13 +25,16 @@ def shard_range(m: int, rank: int, world: int) -> tuple[int, int]:
 
 
 class LocalMoments:
-    """One rank's raw partials: n rows, chain means [m_local, d], tile(k) -> [32, d]."""
+    """One rank's raw partials: n rows, chain means [m_local, d], tile(k) -> [32, d],
+    and optionally all(): every lag [n, d]."""
 
-    def __init__(self, n: int, chain_means: np.ndarray, max_chain_var: np.ndarray, acov_tile):
+    def __init__(self, n: int, chain_means: np.ndarray, max_chain_var: np.ndarray, acov_tile,
+                 acov_all=None):
         self.n = n
         self.chain_means = np.asarray(chain_means, dtype=np.float64)
         self.max_chain_var = np.asarray(max_chain_var, dtype=np.float64)
         self.acov_tile = acov_tile
+        self.acov_all = acov_all
 
 
 def _allreduce(arr: np.ndarray, op, device) -> np.ndarray:
@@ -61,5 +64,8 @@ def allreduce_moments(local: LocalMoments, device="cpu") -> DiagMoments:
     def tile(k: int) -> np.ndarray:
         return _allreduce(local.acov_tile(k), dist.ReduceOp.SUM, device)
 
+    def every_lag() -> np.ndarray:
+        return _allreduce(local.acov_all(), dist.ReduceOp.SUM, device)
+
     return DiagMoments(n=local.n, m=M, d=d, var_means=var_means, max_chain_var=mx,
-                       acov_tile=tile)
+                       acov_tile=tile, acov_all=every_lag if local.acov_all else None)
