@@ -413,7 +413,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
 
     if key != (1 << 64) - 1:
         j = key & ((1 << 24) - 1)
-        kind, label, etick_j, eiter = (int(v) for v in info[j, 2:6])
+        kind, etick_j, label, eiter = (int(v) for v in info[j, 2:6])
         if etick_j <= tick_count:
             raise KernelRunError(chain=j, iteration=eiter, cause=_cause(bundle, kind, label))
     counts_now = info[:, 0]
