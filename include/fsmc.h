@@ -34,8 +34,9 @@ typedef enum {
 } fsmc_status;
 
 /* kernel families: drmh_kernel (kernels/drmh.py:63), elliptical_kernel
- * (kernels/elliptical.py:65), nuts_kernel (kernels/nuts.py:103) */
-enum { FSMC_DRMH = 1, FSMC_ESS = 2, FSMC_NUTS = 3 };
+ * (kernels/elliptical.py:65), nuts_kernel (kernels/nuts.py:103),
+ * slice_kernel (kernels/slice_sampling.py:50) */
+enum { FSMC_DRMH = 1, FSMC_ESS = 2, FSMC_NUTS = 3, FSMC_SLICE = 4 };
 
 /* step variants, lockstep.py:44 STEP_VARIANTS */
 enum { FSMC_PLAIN = 0, FSMC_BUNDLED = 1, FSMC_AMORTIZED = 2 };
@@ -50,7 +51,8 @@ enum {
   FSMC_T_NANBAND = 6,        /* fault injection: std normal, `b` once x[0] > `a` */
   FSMC_T_LOGISTIC = 7,       /* -sum log(1+exp(-y*x)): GP-classification latent (f-space) */
   FSMC_T_FLAT = 8,           /* log density 0 */
-  FSMC_T_LOGREG = 9          /* Bayesian logistic regression, N(0, I) prior (BASELINE config 5) */
+  FSMC_T_LOGREG = 9,         /* Bayesian logistic regression, N(0, I) prior (BASELINE config 5) */
+  FSMC_T_BOX = 10            /* uniform on the box [a, b]^dim: 0 inside, -inf outside */
 };
 
 /* Gaussian-prior split for the elliptical kernel (targets.py:37-42) */
@@ -64,6 +66,9 @@ typedef struct fsmc_kernel {
   int32_t max_depth;            /* nuts */
   int32_t split_body;           /* drmh: 1 = 4-way split proposal (drmh.py:106-156), 6 states */
   double divergence_threshold;  /* nuts */
+  double slice_width;           /* slice: initial bracket width w */
+  int32_t max_expansions;       /* slice: stepping-out budget */
+  int32_t pad;
 } fsmc_kernel;
 
 typedef struct fsmc_target {
@@ -73,7 +78,7 @@ typedef struct fsmc_target {
   int32_t prior_kind;           /* FSMC_PRIOR_* (elliptical kernel only) */
   double log_norm;              /* Gaussian / MoG normaliser, computed as the reference does */
   double a, b;                  /* EQUICORR/MOG: 1/a_perp, 1/(a+d*b); FUNNEL: a = v scale;
-                                   NANBAND: a = threshold, b = value returned */
+                                   NANBAND: a = threshold, b = value returned; BOX: bounds */
   double pad;
   double offsets[FSMC_MAX_MODES];  /* MOG mode offsets (mode k = offsets[k] * 1) */
   const double* mean;           /* [dim] or NULL (zero mean) */

@@ -172,6 +172,13 @@ static double np_logaddexp(double x, double y) {
 static double target_eval(const or_target* t, const double* x, double* g, double* scratch) {
   const int d = t->dim;
   switch (t->kind) {
+    case OR_T_BOX: { /* uniform on [p0, p1]^d */
+      if (g)
+        for (int k = 0; k < d; k++) g[k] = 0.0;
+      for (int k = 0; k < d; k++)
+        if (!(x[k] >= t->p0 && x[k] <= t->p1)) return -INFINITY;
+      return 0.0;
+    }
     case OR_T_FLAT:
       if (g) memset(g, 0, sizeof(double) * d);
       return 0.0;
@@ -321,6 +328,9 @@ typedef struct chain {
   double h0, log_sum_w, sub_log_sum_w;
   int depth, stopped, diverged, direction, sub_stop, n_double, n_check;
   int64_t steps_todo, steps_done;
+  /* slice (slice_sampling.py:29-47) */
+  double s_logy, s_left, s_right, s_lp_left, s_lp_right, s_x1, s_lp_x1, s_lp_x;
+  int s_n_expand, s_n_shrink, s_accepted, s_cap_hits;
 } chain;
 
 static int fail(chain* c, int kind, int label) {
@@ -571,12 +581,83 @@ static int nuts_transition(chain* c, int s) {
   return 1;
 }
 
+
+/* ----------------------------------------------------------------- slice */
+/* kernels/slice_sampling.py:50-156; _logp failures carry the label "slice" (7) */
+#define SLICE_LABEL 7
+static int slice_logp(chain* c, double v, double* out) {
+  double lp = target_eval(c->t, &v, NULL, c->scratch);
+  if (bad_lp(lp)) return fail(c, ERR_BLOCK, SLICE_LABEL);
+  *out = lp;
+  return 0;
+}
+static int slice_expand_continue(chain* c) { /* slice_sampling.py:86-88 */
+  return (c->s_lp_left > c->s_logy || c->s_lp_right > c->s_logy) &&
+         c->s_n_expand < c->k->max_expansions;
+}
+static int slice_block(chain* c, int s) {
+  const double w = c->k->slice_width;
+  if (s == 1) { /* _init_expand, slice_sampling.py:62-74 */
+    c->n_inner = 0;
+    c->s_n_expand = 0;
+    c->s_n_shrink = 0;
+    c->s_accepted = 0;
+    double u = rng_uniform(&c->r);
+    c->s_logy = c->s_lp_x + log(1.0 - u);
+    u = rng_uniform(&c->r);
+    double x0 = c->x[0];
+    c->s_left = x0 - w * u;
+    c->s_right = c->s_left + w;
+    if (slice_logp(c, c->s_left, &c->s_lp_left)) return -1;
+    if (slice_logp(c, c->s_right, &c->s_lp_right)) return -1;
+  } else if (s == 2) { /* _expand, slice_sampling.py:76-84 */
+    c->n_inner++;
+    c->s_n_expand++;
+    if (c->s_lp_left > c->s_logy) {
+      c->s_left -= w;
+      if (slice_logp(c, c->s_left, &c->s_lp_left)) return -1;
+    } else {
+      c->s_right += w;
+      if (slice_logp(c, c->s_right, &c->s_lp_right)) return -1;
+    }
+    if (c->s_n_expand == c->k->max_expansions &&
+        (c->s_lp_left > c->s_logy || c->s_lp_right > c->s_logy))
+      c->s_cap_hits++;
+  } else if (s == 4) { /* _shrink, slice_sampling.py:93-104 */
+    c->n_inner++;
+    c->s_n_shrink++;
+    double u = rng_uniform(&c->r);
+    c->s_x1 = c->s_left + u * (c->s_right - c->s_left);
+    if (slice_logp(c, c->s_x1, &c->s_lp_x1)) return -1;
+    if (c->s_lp_x1 > c->s_logy)
+      c->s_accepted = 1;
+    else if (c->s_x1 < c->x[0])
+      c->s_left = c->s_x1;
+    else
+      c->s_right = c->s_x1;
+  } else if (s == 5) { /* _done, slice_sampling.py:109-112 */
+    c->x[0] = c->s_x1;
+    c->s_lp_x = c->s_lp_x1;
+  } /* s == 3: INIT-S is empty_block */
+  return 0;
+}
+/* fsm.py:323-331: compose_sequential of two single loops */
+static int slice_transition(chain* c, int s) {
+  if (s == 1 || s == 2) return slice_expand_continue(c) ? 2 : 3;
+  if (s == 3 || s == 4) return c->s_accepted ? 5 : 4;
+  return 1;
+}
+
 /* ---------------------------------------------------------- FSM glue */
-int or_n_states(const or_kernel* k) { return k->family == OR_NUTS ? 5 : 3; }
+int or_n_states(const or_kernel* k) { return (k->family == OR_NUTS || k->family == OR_SLICE) ? 5 : 3; }
 int or_loop_states(const or_kernel* k, int32_t* st) {
   if (k->family == OR_NUTS) {
     st[0] = 2; st[1] = 3; st[2] = 4;
     return 3;
+  }
+  if (k->family == OR_SLICE) {
+    st[0] = 2; st[1] = 4;
+    return 2;
   }
   st[0] = 2;
   return 1;
@@ -585,6 +666,7 @@ static int run_block(chain* c, int s) {
   switch (c->k->family) {
     case OR_DRMH: return drmh_block(c, s);
     case OR_ESS: return ess_block(c, s);
+    case OR_SLICE: return slice_block(c, s);
     default: return nuts_block(c, s);
   }
 }
@@ -592,6 +674,7 @@ static int transition(chain* c, int s) {
   switch (c->k->family) {
     case OR_DRMH: return drmh_transition(c, s);
     case OR_ESS: return ess_transition(c, s);
+    case OR_SLICE: return slice_transition(c, s);
     default: return nuts_transition(c, s);
   }
 }
@@ -673,6 +756,15 @@ static int chain_init(run_ctx* ctx, chain* c, int64_t j) {
     c->logy = c->lp_fx;
     memcpy(c->xprop, c->x, sizeof(double) * d);
     c->lp_fprop = c->lp_fx;
+  } else if (ctx->k->family == OR_SLICE) { /* SliceLocals.__init__, slice_sampling.py:33-47 */
+    c->s_lp_x = target_eval(ctx->t, c->x, NULL, c->scratch);
+    if (bad_lp(c->s_lp_x)) return fail(c, ERR_INIT, 1);
+    if (c->s_lp_x == -INFINITY) return fail(c, ERR_ZERO_START, -1);
+    c->s_logy = c->s_lp_x;
+    c->s_left = c->s_right = c->x[0];
+    c->s_lp_left = c->s_lp_right = c->s_lp_x;
+    c->s_x1 = c->x[0];
+    c->s_lp_x1 = c->s_lp_x;
   } else {
     memcpy(c->xprop, c->x, sizeof(double) * d);
     c->sub_log_sum_w = -INFINITY;
@@ -912,6 +1004,15 @@ static int monolithic(run_ctx* ctx, chain* c, int64_t* execs) {
     }
     ess_block(c, 3);
     execs[0] = n_shrink;
+  } else if (fam == OR_SLICE) { /* slice_sampling.py:135-143 */
+    if (slice_block(c, 1)) return -1;
+    while (slice_expand_continue(c))
+      if (slice_block(c, 2)) return -1;
+    while (!c->s_accepted)
+      if (slice_block(c, 4)) return -1;
+    slice_block(c, 5);
+    execs[0] = c->s_n_expand;
+    execs[1] = c->s_n_shrink;
   } else {
     if (nuts_block(c, 1)) return -1;
     while (nuts_outer(c)) {

@@ -18,7 +18,7 @@
 extern "C" {
 #endif
 
-enum { OR_DRMH = 1, OR_ESS = 2, OR_NUTS = 3 };
+enum { OR_DRMH = 1, OR_ESS = 2, OR_NUTS = 3, OR_SLICE = 4 };
 enum { OR_PLAIN = 0, OR_BUNDLED = 1, OR_AMORTIZED = 2 };
 
 /* target kinds (log-density plugin restatements, targets.py) */
@@ -29,7 +29,8 @@ enum {
   OR_T_NANBAND = 4,   /* fault-injection standard normal (make_golden.py) */
   OR_T_LOGISTIC = 5,  /* -sum logaddexp(0, -y*x)  (GP-classification f-space) */
   OR_T_FLAT = 6,      /* log_density = 0 */
-  OR_T_LOGREG = 7     /* Bayesian logistic regression, N(0, I) prior (make_golden.py logreg_target) */
+  OR_T_LOGREG = 7,    /* Bayesian logistic regression, N(0, I) prior (make_golden.py logreg_target) */
+  OR_T_BOX = 8        /* 0 on [p0, p1]^d, -inf outside (pkg/tests/test_kernels.py:205-212) */
 };
 
 typedef struct or_target {
@@ -60,6 +61,9 @@ typedef struct or_kernel {
   int32_t max_depth;        /* nuts */
   int32_t pad;
   double divergence_threshold;
+  double slice_width;       /* slice: initial width w */
+  int32_t max_expansions;   /* slice */
+  int32_t pad2;
 } or_kernel;
 
 typedef struct or_error {
@@ -67,7 +71,7 @@ typedef struct or_error {
   int64_t iteration;   /* sample index (driver's counts[j]) */
   int64_t tick;
   int32_t kind;        /* 1 BlockFailure(nan/+inf), 2 zero-density start, 3 non-finite grad, 4 init failure */
-  int32_t label;       /* state label index (1..K), 0 = shared, -1 = init */
+  int32_t label;       /* state label index (1..K), 0 = shared, -1 = init, 7 = "slice" */
 } or_error;
 
 typedef struct or_run_out {

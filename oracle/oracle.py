@@ -26,9 +26,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 LOG_2PI = math.log(2.0 * math.pi)
 
-DRMH, ESS, NUTS = 1, 2, 3
+DRMH, ESS, NUTS, SLICE = 1, 2, 3, 4
 VARIANTS = {"plain": 0, "bundled": 1, "amortized": 2}
-T_GAUSS, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, T_LOGREG = 1, 2, 3, 4, 5, 6, 7
+T_GAUSS, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, T_LOGREG, T_BOX = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 def build(force: bool = False) -> str:
@@ -55,7 +55,8 @@ class _Kernel(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int32), ("max_tries", ctypes.c_int32),
                 ("proposal_scale", ctypes.c_double), ("step_size", ctypes.c_double),
                 ("max_depth", ctypes.c_int32), ("pad", ctypes.c_int32),
-                ("divergence_threshold", ctypes.c_double)]
+                ("divergence_threshold", ctypes.c_double), ("slice_width", ctypes.c_double),
+                ("max_expansions", ctypes.c_int32), ("pad2", ctypes.c_int32)]
 
 
 class _Error(ctypes.Structure):
@@ -196,6 +197,11 @@ def flat(d) -> OracleTarget:
     return OracleTarget(T_FLAT, d)
 
 
+def box(d, lo=0.0, hi=1.0) -> OracleTarget:
+    """0 on [lo, hi]^d, -inf outside (pkg/tests/test_kernels.py:205-212)."""
+    return OracleTarget(T_BOX, d, p0=float(lo), p1=float(hi))
+
+
 def logreg(X, y) -> OracleTarget:
     """Bayesian logistic regression, N(0, I) prior (tests/golden/make_golden.py logreg_target)."""
     X = np.ascontiguousarray(np.asarray(X, dtype=float))
@@ -239,7 +245,15 @@ def nuts(step_size, max_depth=10, divergence_threshold=1000.0):
                    divergence_threshold=float(divergence_threshold))
 
 
+def slice_(initial_width, max_expansions=32):
+    """kernels/slice_sampling.py:50"""
+    return _Kernel(family=SLICE, slice_width=float(initial_width),
+                   max_expansions=int(max_expansions))
+
+
 def loop_states(kernel):
+    if kernel.family == SLICE:
+        return (2, 4)
     return (2, 3, 4) if kernel.family == NUTS else (2,)
 
 
@@ -259,7 +273,7 @@ class OracleBudget(RuntimeError):
 
 def _run(fn, kernel, target, m, n, seed, x0, init_jitter, chain_offset, nthreads, extra):
     d = target.dim
-    K = 5 if kernel.family == NUTS else 3
+    K = 5 if kernel.family in (NUTS, SLICE) else 3
     L = len(loop_states(kernel))
     samples = np.zeros((n, m, d))
     loops = np.zeros((L, n, m), dtype=np.int64)
@@ -273,7 +287,9 @@ def _run(fn, kernel, target, m, n, seed, x0, init_jitter, chain_offset, nthreads
     x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
     rc = fn(ctypes.byref(kernel), ctypes.byref(ts), m, seed & (2**64 - 1), chain_offset,
             _ptr(x0a), float(init_jitter), n, *extra, nthreads, ctypes.byref(out))
-    res = {"samples": samples, "iter_counts": loops[1] if kernel.family == NUTS else loops[0],
+    iters = loops[1] if kernel.family == NUTS else (loops[0] + loops[1] if kernel.family == SLICE
+                                                    else loops[0])
+    res = {"samples": samples, "iter_counts": iters,
            "loop_counts": {s: loops[i] for i, s in enumerate(loop_states(kernel))},
            "sample_ticks": ticks, "block_exec_counts": blocks, "tick_count": out.tick_count,
            "native_shared_evals": out.native_shared, "sample_counts": counts,

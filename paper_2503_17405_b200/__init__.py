@@ -16,7 +16,7 @@ from .lockstep import (ChainBatch, CostLedger, CostParams, KernelRunError, TickB
 from .prng import RngKey, key, normal, normal_vec, split, uniform, uniform_block
 from .targets import (GaussianPriorDecomposition, TargetError, TargetModel, conjugate_target,
                       correlated_mog_target, equicorrelated_covariance,
-                      equicorrelated_gaussian_target, funnel_target, gaussian_target,
+                      box_target, equicorrelated_gaussian_target, funnel_target, gaussian_target,
                       gp_classification_target, standard_normal_target)
 from .analysis import EssSummary, effective_sample_size, rhat
 

@@ -19,16 +19,17 @@ FSMC_NINT = 32
 MAX_MODES = 8
 
 # families / variants / targets / priors (fsmc.h)
-DRMH, ESS, NUTS = 1, 2, 3
+DRMH, ESS, NUTS, SLICE = 1, 2, 3, 4
 PLAIN, BUNDLED, AMORTIZED = 0, 1, 2
 T_GAUSS_DIAG, T_GAUSS_DENSE, T_GAUSS_EQUICORR, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, \
-    T_LOGREG = range(1, 10)
+    T_LOGREG, T_BOX = range(1, 11)
 PRIOR_NONE, PRIOR_IDENTITY, PRIOR_DENSE = 0, 1, 2
 
 # per-chain int slots
 I_COUNTER, I_STREAM, I_STATE, I_TICK, I_COUNT = 0, 1, 2, 3, 4
 I_ERR_KIND, I_ERR_LABEL, I_ERR_TICK, I_ERR_ITER = 5, 6, 7, 8
-I_SHARED, I_BLOCKS, I_PEND, I_FAMILY, I_RESUME = 9, 10, 16, 19, 31
+I_SHARED, I_BLOCKS, I_PEND, I_FAMILY, I_RESUME = 9, 10, 16, 20, 31
+SLICE_LABEL = 7   # device label of check_log_density(.., "slice")
 E_NONE, E_BLOCK, E_ZERO_START, E_GRAD, E_INIT = 0, 1, 2, 3, 4
 
 _D = ctypes.c_double
@@ -46,7 +47,8 @@ class EngineError(RuntimeError):
 class Kernel(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int32), ("max_tries", ctypes.c_int32),
                 ("proposal_scale", _D), ("step_size", _D), ("max_depth", ctypes.c_int32),
-                ("split_body", ctypes.c_int32), ("divergence_threshold", _D)]
+                ("split_body", ctypes.c_int32), ("divergence_threshold", _D),
+                ("slice_width", _D), ("max_expansions", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class Target(ctypes.Structure):

@@ -6,6 +6,7 @@
 #define FSMC_DRMH_CONFIGS(X) X(1, 1) X(1, 2) X(1, 4) X(1, 10) X(1, 16) X(2, 5) X(4, 3) X(32, 4)
 #define FSMC_DRMH_SPLIT_CONFIGS(X) X(1, 1) X(1, 2) X(1, 4) X(1, 10) X(32, 4)
 #define FSMC_ESS_CONFIGS(X) X(1, 2) X(1, 4) X(32, 1) X(32, 2) X(32, 4) X(32, 8) X(128, 8)
+#define FSMC_SLICE_CONFIGS(X) X(1, 1)
 #define FSMC_NUTS_CONFIGS(X) X(1, 2) X(2, 2) X(4, 3) X(4, 4) X(8, 2) X(32, 1) X(32, 4) X(128, 2)
 
 // (G, E, plugin) triples compiled with the plugin fixed at compile time: the

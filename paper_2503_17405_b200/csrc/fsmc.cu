@@ -215,6 +215,8 @@ cudaError_t dispatch_ess(int, int, int, Params&, const LaunchCtx&, cudaStream_t,
                          const double*, double);
 cudaError_t dispatch_nuts(int, int, int, Params&, const LaunchCtx&, cudaStream_t, uint64_t, long long,
                           const double*, double);
+cudaError_t dispatch_slice(int, int, int, Params&, const LaunchCtx&, cudaStream_t, uint64_t, long long,
+                           const double*, double);
 }  // namespace fsmc
 
 namespace {
@@ -231,7 +233,13 @@ bool pick_config(int family, int dim, int lanes, GE& out) {
       FSMC_DRMH_CONFIGS(X)};
   static const GE ess[] = {FSMC_ESS_CONFIGS(X)};
   static const GE nuts[] = {FSMC_NUTS_CONFIGS(X)};
+  static const GE slice[] = {FSMC_SLICE_CONFIGS(X)};
 #undef X
+  if (family == FSMC_SLICE) {
+    if (dim != 1 || (lanes > 1)) return false;
+    out = slice[0];
+    return true;
+  }
   const GE* list = family == FSMC_DRMH ? drmh : family == FSMC_ESS ? ess : nuts;
   int cnt = family == FSMC_DRMH ? (int)(sizeof(drmh) / sizeof(GE))
             : family == FSMC_ESS ? (int)(sizeof(ess) / sizeof(GE))
@@ -256,6 +264,11 @@ bool pick_config(int family, int dim, int lanes, GE& out) {
   return true;
 }
 
+int n_states(const fsmc_kernel* k) {
+  if (k->family == FSMC_NUTS || k->family == FSMC_SLICE) return 5;
+  return k->family == FSMC_DRMH && k->split_body ? 6 : 3;
+}
+
 LaunchCtx launch_ctx() {
   LaunchCtx lc;
   lc.num_sms = num_sms();
@@ -269,13 +282,14 @@ cudaError_t dispatch_family(int op, const GE& ge, Params& p, cudaStream_t s, uin
   switch (p.k.family) {
     case FSMC_DRMH: return dispatch_drmh(op, ge.g, ge.e, p, lc, s, ps, off, x0, jit);
     case FSMC_ESS: return dispatch_ess(op, ge.g, ge.e, p, lc, s, ps, off, x0, jit);
+    case FSMC_SLICE: return dispatch_slice(op, ge.g, ge.e, p, lc, s, ps, off, x0, jit);
     default: return dispatch_nuts(op, ge.g, ge.e, p, lc, s, ps, off, x0, jit);
   }
 }
 
 fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_state* st) {
   if (!k || !t || !st) return fail(FSMC_ERR_ARG, "null argument");
-  if (k->family < FSMC_DRMH || k->family > FSMC_NUTS) return fail(FSMC_ERR_ARG, "unknown kernel family");
+  if (k->family < FSMC_DRMH || k->family > FSMC_SLICE) return fail(FSMC_ERR_ARG, "unknown kernel family");
   if (t->dim < 1) return fail(FSMC_ERR_ARG, "dim must be >= 1");
   if (st->dim != t->dim) return fail(FSMC_ERR_ARG, "state dim does not match target dim");
   if (st->m < 1 || st->m >= (1LL << 24)) return fail(FSMC_ERR_ARG, "m must be in [1, 2^24) per state block");
@@ -283,6 +297,10 @@ fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_st
     return fail(FSMC_ERR_ARG, "invalid drmh parameters");
   if (k->family == FSMC_NUTS && (k->max_depth < 1 || k->max_depth > 40 || !(k->step_size > 0)))
     return fail(FSMC_ERR_ARG, "invalid nuts parameters");
+  if (k->family == FSMC_SLICE && (!(k->slice_width > 0) || k->max_expansions < 0))
+    return fail(FSMC_ERR_ARG, "invalid slice parameters");
+  if (k->family == FSMC_SLICE && t->dim != 1)
+    return fail(FSMC_ERR_ARG, "slice sampling here is univariate");
   if (k->family == FSMC_ESS && t->prior_kind == FSMC_PRIOR_NONE)
     return fail(FSMC_ERR_ARG, "elliptical slice sampling needs a Gaussian-prior split");
   if (t->kind == FSMC_T_MOG && (t->n_modes < 1 || t->n_modes > FSMC_MAX_MODES))
@@ -307,6 +325,7 @@ fsmc_status fsmc_state_layout(const fsmc_kernel* k, int64_t dim, int32_t* n_vec,
       else { *n_vec = 2; *n_scal = 3; *n_loop = 1; *n_states = 3; }
       break;
     case FSMC_ESS: *n_vec = 3; *n_scal = 6; *n_loop = 1; *n_states = 3; break;
+    case FSMC_SLICE: *n_vec = 2; *n_scal = 8; *n_loop = 2; *n_states = 5; break;
     case FSMC_NUTS:
       *n_vec = 12 + 2 * k->max_depth; *n_scal = 3; *n_loop = 3; *n_states = 5;
       break;
@@ -359,7 +378,7 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
   p.tick_limit = tick_limit;
   p.variant = variant;
   p.mode = mode;
-  int K = k->family == FSMC_NUTS ? 5 : (k->family == FSMC_DRMH && k->split_body ? 6 : 3);
+  int K = n_states(k);
   for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
   cudaStream_t cs = (cudaStream_t)stream_;
   p.next_chain = scratch().words;
@@ -388,7 +407,7 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
   p.tick_limit = tick_limit;
   p.variant = variant;
   p.mode = mode;
-  int K = k->family == FSMC_NUTS ? 5 : (k->family == FSMC_DRMH && k->split_body ? 6 : 3);
+  int K = n_states(k);
   for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
   p.b_lp = lp;
   p.b_grad = grad;

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
       for (int e = 0; e < E; e++) f.x[e] = f.x[e] + jitter * eps[e];
     }
     bool ok = true;
-    if constexpr (F<G, E>::K == 5) {
+    if constexpr (F<G, E>::SHAPE == SHAPE_NESTED) {
       f.init_state();
       f.ck = nullptr;
     } else {
@@ -189,7 +189,7 @@ __device__ __forceinline__ bool grid_any(const Params& p, bool pred, unsigned& p
 }
 
 // vmap semantics of each kernel's monolithic sampler (drmh.py:163-169,
-// elliptical.py:122-132, nuts.py:237-248): every while-loop test is a
+// elliptical.py:122-132, nuts.py:237-248, slice_sampling.py:135-143): every while-loop test is a
 // barrier across all chains of the wave, so a sample costs max over chains of
 // its loop count.  Written as a uniform program counter so the state body
 // (and its log-density evaluation) is instantiated once.
@@ -223,7 +223,17 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
       if (pc == PC_INIT) {
         s = 1;
         pc = PC_OUTER;
-      } else if constexpr (FF::K == 5) {
+      } else if constexpr (FF::SHAPE == SHAPE_SEQ) {
+        if (pc == PC_OUTER) {  // while _expand_continue(z)
+          bool co = live && f.loop_continue(p);
+          if (grid_any(p, co, phase)) s = co ? 2 : 0;
+          else { s = 3; pc = PC_INNER; }
+        } else {  // while _shrink_continue(z)
+          bool ci = live && f.loop2_continue();
+          if (grid_any(p, ci, phase)) s = ci ? 4 : 0;
+          else { s = 5; pc = PC_END; }
+        }
+      } else if constexpr (FF::SHAPE == SHAPE_NESTED) {
         if (pc == PC_OUTER) {  // while _outer_continue(z)
           bool co = live && f.outer_continue(p);
           if (!grid_any(p, co, phase)) { s = 5; pc = PC_END; }
@@ -239,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
         else { s = FF::K; pc = PC_END; }
       }
       // one while-loop body: PROPOSE, or the split body's states 2..K-1
-      const int s_last = (s == 2 && FF::K == 6) ? 5 : s;
+      const int s_last = (s == 2 && FF::SHAPE == SHAPE_SPLIT) ? 5 : s;
 #pragma unroll 1
       for (int ss = s; live && s && ss <= s_last; ss++) {
         bool did = false;

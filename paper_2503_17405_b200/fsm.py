@@ -129,7 +129,7 @@ def compose_single_loop(labels=("INIT", "BODY", "DONE"), shared=None, family=0) 
                          loop_states=frozenset({2}), shared=shared, family=family)
 
 
-def compose_sequential(f1: FsmDefinition, f2: FsmDefinition) -> FsmDefinition:
+def compose_sequential(f1: FsmDefinition, f2: FsmDefinition, family: int = 0) -> FsmDefinition:
     """Two single-loop machines back to back -> five states (fsm.py:307-345)."""
     if f1.n_states != 3 or f2.n_states != 3:
         raise FsmError("sequential composition expects two single-loop machines")
@@ -138,7 +138,7 @@ def compose_sequential(f1: FsmDefinition, f2: FsmDefinition) -> FsmDefinition:
     return FsmDefinition(labels=(*f1.labels, f2.labels[1], f2.labels[2]),
                          edges=frozenset({(1, 2), (1, 3), (2, 2), (2, 3), (3, 4), (3, 5),
                                           (4, 4), (4, 5), (5, 1)}),
-                         loop_states=frozenset({2, 4}))
+                         loop_states=frozenset({2, 4}), family=family)
 
 
 def compose_nested(inner: FsmDefinition, labels=("INIT", "DONE"), family=0) -> FsmDefinition:

@@ -35,6 +35,8 @@ class KernelBundle:
     max_depth: int = 0
     divergence_threshold: float = 1000.0
     split_body: bool = False
+    slice_width: float = 0.0
+    max_expansions: int = 0
 
     def __post_init__(self):
         if not set(self.iter_states) <= self.fsm.loop_states:
@@ -49,6 +51,8 @@ class KernelBundle:
         k.max_depth = self.max_depth
         k.split_body = int(self.split_body)
         k.divergence_threshold = self.divergence_threshold
+        k.slice_width = self.slice_width
+        k.max_expansions = self.max_expansions
         return k
 
     def check_target(self, target) -> None:
@@ -57,6 +61,9 @@ class KernelBundle:
             raise KernelError(f"{self.name}: target lacks the Gaussian-prior decomposition")
         if self.family == _lib.NUTS and not target.has_gradient:
             raise KernelError(f"{self.name}: target lacks a gradient")
+        if self.family == _lib.SLICE and target.dim != 1:   # slice_sampling.py:128-132
+            raise KernelError(f"{self.name}: slice sampling here is univariate, target has dim "
+                              f"{target.dim}")
 
     @property
     def loop_states(self) -> tuple:

@@ -258,9 +258,12 @@ def _cause(bundle, kind: int, label: int) -> Exception:
         return KernelError("starting point has zero density")
     if kind == _lib.E_GRAD:
         return KernelError("non-finite gradient")
-    if kind == _lib.E_INIT:
-        return BlockFailure("INIT", "log-density evaluated to a non-finite value (NaN or +inf)")
-    name = "shared log f" if label == 0 else labels[label - 1]
+    if kind == _lib.E_INIT:     # the Locals constructor's check (e.g. drmh.py:45, slice_sampling.py:38)
+        return BlockFailure(labels[0], "log-density evaluated to a non-finite value (NaN or +inf)")
+    if label == _lib.SLICE_LABEL:
+        name = "slice"
+    else:
+        name = "shared log f" if label == 0 else labels[label - 1]
     return BlockFailure(name, "log-density evaluated to a non-finite value (NaN or +inf)")
 
 

@@ -263,6 +263,14 @@ def nan_band_target(d: int, threshold: float, value: float) -> TargetModel:
     return TargetModel(f"nanband-{d}d", d, _lib.T_NANBAND, a=float(threshold), b=float(value))
 
 
+def box_target(d: int, lo: float = 0.0, hi: float = 1.0) -> TargetModel:
+    """Uniform on [lo, hi]^d: log density 0 inside, -inf outside (the compact-support
+    target of the reference's slice tests, tests/test_kernels.py:205-212)."""
+    if not hi > lo:
+        raise TargetError(f"empty box [{lo}, {hi}]")
+    return TargetModel(f"box-{d}d", d, _lib.T_BOX, a=float(lo), b=float(hi))
+
+
 def flat_target(d: int) -> TargetModel:
     return TargetModel(f"flat-{d}d", d, _lib.T_FLAT)
 

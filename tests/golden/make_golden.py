@@ -25,7 +25,7 @@ sys.path.insert(0, REF + "/src")
 sys.path.insert(0, REF + "/tests")
 
 from fsm_mcmc import prng  # noqa: E402
-from fsm_mcmc.kernels import drmh_kernel, elliptical_kernel, nuts_kernel  # noqa: E402
+from fsm_mcmc.kernels import drmh_kernel, elliptical_kernel, nuts_kernel, slice_kernel  # noqa: E402
 from fsm_mcmc.lockstep import (KernelRunError, TickBudgetExceeded,  # noqa: E402
                                init_batch, run_fsm_batched, run_standard_batched)
 from fsm_mcmc.targets import (GaussianPriorDecomposition, TargetModel,  # noqa: E402
@@ -136,18 +136,20 @@ def ledger_dict(prefix, samples, led, out):
 
 
 def run_case(name, bundle, target, m, n, seed, variants, extra=None, tick_chunk=100,
-             standard=True):
+             standard=True, x0=None):
     out = {"m": np.int64(m), "n": np.int64(n), "seed": np.int64(seed),
            "tick_chunk": np.int64(tick_chunk)}
+    if x0 is not None:
+        out["x0"] = np.asarray(x0, dtype=float)
     if extra:
         out.update(extra)
     for v in variants:
-        s, led = run_fsm_batched(bundle, target, init_batch(bundle, target, m, seed), n,
+        s, led = run_fsm_batched(bundle, target, init_batch(bundle, target, m, seed, x0=x0), n,
                                  step_variant=v, record_sample_ticks=True,
                                  tick_chunk=tick_chunk)
         ledger_dict(f"{v}_", s, led, out)
     if standard:
-        s, led = run_standard_batched(bundle, target, init_batch(bundle, target, m, seed), n)
+        s, led = run_standard_batched(bundle, target, init_batch(bundle, target, m, seed, x0=x0), n)
         ledger_dict("standard_", s, led, out)
     np.savez_compressed(os.path.join(OUT, name + ".npz"), **out)
     print("wrote", name, {k: getattr(v, "shape", ()) for k, v in out.items() if "samples" in k})
@@ -245,6 +247,7 @@ def main():
     run_case("nuts_logreg512x16", nuts_kernel(0.1, 8), logreg_target(X, y),
              m=6, n=40, seed=9, variants=("plain", "bundled"), extra={"X": X, "y": y})
     main_split_only()
+    main_slice_only()
 
 
 def main_split_only():
@@ -254,6 +257,43 @@ def main_split_only():
     run_case("drmh_split_mog10", drmh_kernel(100, 0.1, split_body=True),
              correlated_mog_target(10, 0.9, [-3.0, 0.0, 3.0]), m=8, n=40, seed=6,
              variants=("plain", "bundled"))
+
+
+def main_slice_only():
+    """The univariate slice sampler (slice_sampling.py): stepping-out and
+    shrinkage counts, the expansion cap, compact support, and failures."""
+    std1 = gaussian_target(np.zeros(1), np.eye(1))
+    run_case("slice_std1", slice_kernel(1.0), std1, m=8, n=200, seed=10,
+             variants=("plain", "bundled", "amortized"), tick_chunk=1)
+    run_case("slice_narrow", slice_kernel(0.2, max_expansions=50),
+             gaussian_target(np.array([1.5]), np.array([[2.0]])), m=6, n=120, seed=11,
+             variants=("plain", "bundled"), tick_chunk=10)
+    run_case("slice_cap", slice_kernel(0.05, max_expansions=3), std1, m=6, n=100, seed=12,
+             variants=("plain", "bundled"))
+
+    def uniform01(x):
+        return 0.0 if 0.0 <= float(x[0]) <= 1.0 else -math.inf
+    box = TargetModel(name="uniform01", dim=1, log_density=uniform01)
+    run_case("slice_box", slice_kernel(10.0, max_expansions=8), box, m=4, n=200, seed=9,
+             variants=("plain", "bundled"), x0=np.array([0.5]))
+    out = {}
+    t = nan_band_target(1, 2.0, math.nan)
+    b = slice_kernel(1.0)
+    for v in ("plain", "bundled"):
+        try:
+            run_fsm_batched(b, t, init_batch(b, t, 6, 3), 400, step_variant=v)
+            raise SystemExit("expected a failure")
+        except KernelRunError as e:
+            out[f"nan_{v}"] = np.array([e.chain, e.iteration])
+            out[f"nan_{v}_label"] = np.array(e.cause.label)
+    try:
+        run_standard_batched(b, t, init_batch(b, t, 6, 3), 400)
+        raise SystemExit("expected a failure")
+    except KernelRunError as e:
+        out["nan_standard"] = np.array([e.chain, e.iteration])
+        out["nan_standard_label"] = np.array(e.cause.label)
+    np.savez_compressed(os.path.join(OUT, "errors_slice.npz"), **out)
+    print("wrote errors_slice", out)
 
 
 def main_logreg_only():
@@ -267,5 +307,7 @@ if __name__ == "__main__":
         main_logreg_only()
     elif len(sys.argv) > 1 and sys.argv[1] == "split":
         main_split_only()
+    elif len(sys.argv) > 1 and sys.argv[1] == "slice":
+        main_slice_only()
     else:
         main()

@@ -33,14 +33,25 @@ CASES = {
     "nuts_logreg512x16": (("plain", "bundled", "standard"), ("nuts", 0.1, 8, 1000.0), ("logreg",)),
     "drmh_split_std1": (("plain", "bundled", "standard"), ("drmh-split", 50, 0.4), ("gauss", np.zeros(1), np.eye(1))),
     "drmh_split_mog10": (("plain", "bundled", "standard"), ("drmh-split", 100, 0.1), ("mog", 10, 0.9, (-3.0, 0.0, 3.0))),
+    "slice_std1": (("plain", "bundled", "amortized", "standard"), ("slice", 1.0, 32), ("gauss", np.zeros(1), np.eye(1))),
+    "slice_narrow": (("plain", "bundled", "standard"), ("slice", 0.2, 50), ("gauss", np.array([1.5]), np.array([[2.0]]))),
+    "slice_cap": (("plain", "bundled", "standard"), ("slice", 0.05, 3), ("gauss", np.zeros(1), np.eye(1))),
+    "slice_box": (("plain", "bundled", "standard"), ("slice", 10.0, 8), ("box", 1, 0.0, 1.0)),
 }
 
 # cases the oracle does not restate (checked against the goldens on the device only)
 DEVICE_ONLY = {"drmh_split_std1", "drmh_split_mog10"}
 
 
+def x0_of(g):
+    """The case's start point (None: the default zeros)."""
+    return g["x0"] if "x0" in g.files else None
+
+
 def oracle_kernel(spec):
     from oracle import oracle as O
+    if spec[0] == "slice":
+        return O.slice_(spec[1], spec[2])
     if spec[0] == "drmh":
         return O.drmh(spec[1], spec[2])
     if spec[0] == "ess":
@@ -55,6 +66,8 @@ def oracle_target(spec):
         return O.mog(spec[1], spec[2], list(spec[3]))
     if kind == "funnel":
         return O.funnel(spec[1])
+    if kind == "box":
+        return O.box(spec[1], spec[2], spec[3])
     if kind == "gauss":
         return O.gaussian(spec[1], spec[2])
     if kind == "equicorr":
@@ -74,6 +87,8 @@ def device_kernel(spec):
     import paper_2503_17405_b200 as fm
     if spec[0] == "drmh-split":
         return fm.drmh_kernel(spec[1], spec[2], split_body=True)
+    if spec[0] == "slice":
+        return fm.slice_kernel(spec[1], spec[2])
     if spec[0] == "drmh":
         return fm.drmh_kernel(spec[1], spec[2])
     if spec[0] == "ess":
@@ -89,6 +104,8 @@ def device_target(spec, structure="auto"):
         return fm.correlated_mog_target(spec[1], spec[2], list(spec[3]))
     if kind == "funnel":
         return fm.funnel_target(spec[1])
+    if kind == "box":
+        return fm.box_target(spec[1], spec[2], spec[3])
     if kind == "gauss":
         return fm.gaussian_target(spec[1], spec[2], structure=structure)
     if kind == "equicorr":

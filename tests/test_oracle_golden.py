@@ -8,7 +8,7 @@ import math
 import numpy as np
 import pytest
 
-from golden_cases import CASES, DEVICE_ONLY, load, oracle_kernel, oracle_target, rel_err
+from golden_cases import CASES, DEVICE_ONLY, load, oracle_kernel, oracle_target, rel_err, x0_of
 from oracle import oracle as O
 
 SAMPLE_TOL = 1e-12
@@ -44,11 +44,12 @@ def test_oracle_matches_reference(name):
     g = load(name)
     m, n, seed, chunk = (int(g[k]) for k in ("m", "n", "seed", "tick_chunk"))
     kern, targ = oracle_kernel(kspec), oracle_target(tspec)
+    x0 = x0_of(g)
     for v in variants:
         if v == "standard":
-            r = O.run_standard(kern, targ, m, n, seed)
+            r = O.run_standard(kern, targ, m, n, seed, x0=x0)
         else:
-            r = O.run_fsm(kern, targ, m, n, seed, variant=v, tick_chunk=chunk, nthreads=4)
+            r = O.run_fsm(kern, targ, m, n, seed, variant=v, tick_chunk=chunk, nthreads=4, x0=x0)
         assert np.array_equal(r["iter_counts"], g[v + "_iter_counts"]), v
         for s, mat in r["loop_counts"].items():
             assert np.array_equal(mat, g[f"{v}_loop_{s}"]), (v, s)
@@ -76,6 +77,26 @@ def test_oracle_errors_match_reference():
     assert r["tick_count"] == int(e["budget_tick_count"])
     assert list(r["sample_counts"]) == list(e["budget_sample_counts"])
     assert np.array_equal(r["iter_counts"], e["budget_iter_counts"])
+
+
+def test_oracle_slice_errors_match_reference():
+    e = load("errors_slice")
+    for v in ("plain", "bundled"):
+        with pytest.raises(O.OracleError) as info:
+            O.run_fsm(O.slice_(1.0), O.nanband(1, 2.0, math.nan), 6, 400, 3, variant=v)
+        assert [info.value.chain, info.value.iteration] == list(e[f"nan_{v}"])
+        assert info.value.label == 7 and str(e[f"nan_{v}_label"]) == "slice"
+    with pytest.raises(O.OracleError) as info:
+        O.run_standard(O.slice_(1.0), O.nanband(1, 2.0, math.nan), 6, 400, 3)
+    assert [info.value.chain, info.value.iteration] == list(e["nan_standard"])
+
+
+def test_oracle_slice_cap_hits_expansion_budget():
+    """slice_cap: the stepping-out budget (3) binds in some samples and EXPAND
+    never runs more often than the budget (slice_sampling.py:83-88)."""
+    g = load("slice_cap")
+    assert g["plain_loop_2"].max() == 3
+    assert np.array_equal(g["plain_iter_counts"], g["plain_loop_2"] + g["plain_loop_4"])
 
 
 def test_oracle_threads_and_shards_are_exact():
