@@ -218,3 +218,15 @@ def rhat_from_moments(mom: DiagMoments) -> np.ndarray:
 def rhat(chains, burn: int = 0) -> np.ndarray:
     """Gelman-Rubin R-hat per dimension of an (n, m, d) array."""
     return rhat_from_moments(diag_moments(chains, burn))
+
+
+# the cost-theory half of the reference module (analysis.py:53-324)
+from .efficiency import (BoundEstimate, ConcentrationReport, EfficiencyReport,  # noqa: E402
+                         PropBoundReport, barrier_cost, bernoulli_bound_closed_form, bound_R,
+                         concentration_check, desync_cost, efficiency_model, efficiency_report,
+                         hoeffding_rate, verify_prop_bound)
+
+__all__ += ["barrier_cost", "desync_cost", "efficiency_model", "efficiency_report",
+            "EfficiencyReport", "bound_R", "BoundEstimate", "bernoulli_bound_closed_form",
+            "verify_prop_bound", "PropBoundReport", "concentration_check", "ConcentrationReport",
+            "hoeffding_rate"]

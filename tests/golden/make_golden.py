@@ -248,6 +248,7 @@ def main():
              m=6, n=40, seed=9, variants=("plain", "bundled"), extra={"X": X, "y": y})
     main_split_only()
     main_slice_only()
+    main_efficiency_only()
 
 
 def main_split_only():
@@ -296,6 +297,35 @@ def main_slice_only():
     print("wrote errors_slice", out)
 
 
+def main_efficiency_only():
+    """Cost-theory analytics (analysis.py:53-324) on fixed inputs."""
+    from fsm_mcmc import analysis as A
+    from fsm_mcmc.lockstep import CostParams
+    out = {}
+    rng = np.random.default_rng(77)
+    N = rng.geometric(0.2, size=(300, 64)).astype(np.int64)
+    out["N"] = N
+    out["barrier"] = np.float64(A.barrier_cost(N))
+    out["desync"] = np.float64(A.desync_cost(N))
+    params = CostParams(block_costs=(0.05, 1.0, 0.05), alpha=1.0, loop_states=(2,))
+    rep = A.efficiency_report(params, N, standard_cost_per_sample=3.0, fsm_cost_per_sample=1.5)
+    out["report"] = np.array([rep.m, rep.E_of_m, rep.R_of_m, rep.mean_N, rep.mean_max_N])
+    for m in (1, 16, 1024):
+        b = A.bound_R(m, samples=N.reshape(-1), n_replicates=2000, seed=5)
+        out[f"bound_{m}"] = np.array([b.estimate, b.std_error])
+    b = A.bound_R(16, bernoulli=(0.1, 3.0), n_replicates=20_000, seed=1)
+    out["bound_bern"] = np.array([b.estimate, b.std_error, b.closed_form])
+    rep = A.verify_prop_bound(500, seed=3)
+    out["prop"] = np.array([len(rep.violations), rep.tightness_cases, rep.tightness_max_rel_err,
+                            rep.max_excess])
+    runs = [rng.geometric(0.4, size=(4000, 8)) for _ in range(6)]
+    out["conc_runs"] = np.stack(runs)
+    c = A.concentration_check(runs, (10, 100, 1000, 4000), params)
+    out["conc"] = np.array([c.slope, c.slope_stderr, c.limit_estimate, *c.deviations])
+    np.savez_compressed(os.path.join(OUT, "efficiency.npz"), **out)
+    print("wrote efficiency")
+
+
 def main_logreg_only():
     X, y = logreg_data(512, 16, seed=0)
     run_case("nuts_logreg512x16", nuts_kernel(0.1, 8), logreg_target(X, y),
@@ -309,5 +339,7 @@ if __name__ == "__main__":
         main_split_only()
     elif len(sys.argv) > 1 and sys.argv[1] == "slice":
         main_slice_only()
+    elif len(sys.argv) > 1 and sys.argv[1] == "efficiency":
+        main_efficiency_only()
     else:
         main()
