@@ -52,7 +52,8 @@ enum {
   FSMC_T_LOGISTIC = 7,       /* -sum log(1+exp(-y*x)): GP-classification latent (f-space) */
   FSMC_T_FLAT = 8,           /* log density 0 */
   FSMC_T_LOGREG = 9,         /* Bayesian logistic regression, N(0, I) prior (BASELINE config 5) */
-  FSMC_T_BOX = 10            /* uniform on the box [a, b]^dim: 0 inside, -inf outside */
+  FSMC_T_BOX = 10,           /* uniform on the box [a, b]^dim: 0 inside, -inf outside */
+  FSMC_T_GP_HYPER = 11       /* squared-exponential GP hyperparameters (sigma, tau, lam)  targets.py:191-265 */
 };
 
 /* Gaussian-prior split for the elliptical kernel (targets.py:37-42) */
@@ -78,8 +79,11 @@ typedef struct fsmc_target {
   int32_t prior_kind;           /* FSMC_PRIOR_* (elliptical kernel only) */
   double log_norm;              /* Gaussian / MoG normaliser, computed as the reference does */
   double a, b;                  /* EQUICORR/MOG: 1/a_perp, 1/(a+d*b); FUNNEL: a = v scale;
-                                   NANBAND: a = threshold, b = value returned; BOX: bounds */
-  double pad;
+                                   NANBAND: a = threshold, b = value returned; BOX: bounds;
+                                   GP_HYPER: a = jitter */
+  int32_t full;                 /* set by the library: 1 = the full log density, 0 = the
+                                   Gaussian-prior residual (elliptical kernel) */
+  int32_t scratch;              /* extra shared-memory doubles per chain the plugin needs */
   double offsets[FSMC_MAX_MODES];  /* MOG mode offsets (mode k = offsets[k] * 1) */
   const double* mean;           /* [dim] or NULL (zero mean) */
   const double* diag;           /* [dim] GAUSS_DIAG: diagonal of L^-1 (dim 1: unused) */
@@ -88,7 +92,8 @@ typedef struct fsmc_target {
   const double* mat2_t;         /* [dim*dim] GAUSS_DENSE: precision^T row-major */
   const double* yvec;           /* [dim] LOGISTIC labels (+-1) */
   const double* prior_t;        /* [dim*dim] PRIOR_DENSE: L^T row-major (L lower-triangular) */
-  const double* data;           /* [n_rows*dim] LOGREG design matrix, row-major (labels in yvec) */
+  const double* data;           /* LOGREG: [n_rows*dim] design matrix, row-major (labels in yvec);
+                                   GP_HYPER: [n_rows*n_rows] squared distances (outputs in yvec) */
   int64_t n_rows;
 } fsmc_target;
 
@@ -123,7 +128,8 @@ enum {
   FSMC_I_RESUME = 31 /* batched mode: suspended-at-evaluation record */
 };
 /* error kinds in FSMC_I_ERR_KIND */
-enum { FSMC_E_NONE = 0, FSMC_E_BLOCK = 1, FSMC_E_ZERO_START = 2, FSMC_E_GRAD = 3, FSMC_E_INIT = 4 };
+enum { FSMC_E_NONE = 0, FSMC_E_BLOCK = 1, FSMC_E_ZERO_START = 2, FSMC_E_GRAD = 3, FSMC_E_INIT = 4,
+       FSMC_E_TARGET = 5 /* the plugin itself failed (TargetError, e.g. a kernel matrix not PD) */ };
 
 int32_t fsmc_abi_version(void);
 const char* fsmc_last_error(void);

@@ -172,6 +172,83 @@ static double np_logaddexp(double x, double y) {
 static double target_eval(const or_target* t, const double* x, double* g, double* scratch) {
   const int d = t->dim;
   switch (t->kind) {
+    case OR_T_GP: { /* targets.py:191-265 with LAPACK's operation order (dpotf2, dpotrs) */
+      const int n = (int)t->n_rows;
+      const double sigma = x[0], tau = x[1], lam = x[2];
+      double* K = (double*)malloc(sizeof(double) * (size_t)n * (3 * n + 2));
+      double* Ex = K + (size_t)n * n;
+      double* Ki = Ex + (size_t)n * n;
+      double* al = Ki + (size_t)n * n;
+      double* tmp = al + n;
+      const double nl2 = -(lam * lam), t2 = tau * tau, dg = sigma * sigma + t->p0;
+      for (int i = 0; i < n; i++)
+        for (int j = 0; j < n; j++) {
+          Ex[i * n + j] = exp(nl2 * t->data[i * n + j]);
+          K[i * n + j] = t2 * Ex[i * n + j] + (i == j ? dg : 0.0);
+        }
+      /* left-looking Cholesky (dpotf2, lower) */
+      for (int j = 0; j < n; j++) {
+        double ajj = K[j * n + j];
+        for (int k = 0; k < j; k++) ajj -= K[j * n + k] * K[j * n + k];
+        if (!(ajj > 0.0)) { free(K); return NAN; }
+        ajj = sqrt(ajj);
+        K[j * n + j] = ajj;
+        const double r = 1.0 / ajj;
+        for (int i = j + 1; i < n; i++) {
+          double a = K[i * n + j];
+          for (int k = 0; k < j; k++) a -= K[i * n + k] * K[j * n + k];
+          K[i * n + j] = a * r;
+        }
+      }
+      /* alpha = K^-1 y (dpotrs: L z = y column-oriented, L^T alpha = z dot-form) */
+      for (int i = 0; i < n; i++) al[i] = t->yvec[i];
+      for (int k = 0; k < n; k++) {
+        al[k] /= K[k * n + k];
+        for (int i = k + 1; i < n; i++) al[i] -= al[k] * K[i * n + k];
+      }
+      for (int i = n - 1; i >= 0; i--) {
+        double tv = al[i];
+        for (int k = i + 1; k < n; k++) tv -= K[k * n + i] * al[k];
+        al[i] = tv / K[i * n + i];
+      }
+      double q = 0.0, ld = 0.0;
+      for (int i = 0; i < n; i++) {
+        q += t->yvec[i] * al[i];
+        ld += log(K[i * n + i]);
+      }
+      const double logdet = 2.0 * ld;
+      const double lml = -0.5 * q - 0.5 * logdet - 0.5 * n * LOG_2PI;
+      if (g) {
+        /* K^-1 = cho_solve(cf, eye) column by column, then A = alpha alpha^T - K^-1 */
+        for (int c = 0; c < n; c++) {
+          for (int i = 0; i < n; i++) tmp[i] = (i == c) ? 1.0 : 0.0;
+          for (int k = 0; k < n; k++) {
+            tmp[k] /= K[k * n + k];
+            for (int i = k + 1; i < n; i++) tmp[i] -= tmp[k] * K[i * n + k];
+          }
+          for (int i = n - 1; i >= 0; i--) {
+            double tv = tmp[i];
+            for (int k = i + 1; k < n; k++) tv -= K[k * n + i] * tmp[k];
+            tmp[i] = tv / K[i * n + i];
+          }
+          for (int i = 0; i < n; i++) Ki[i * n + c] = tmp[i];
+        }
+        double tr = 0.0, se = 0.0, sed = 0.0;
+        for (int i = 0; i < n; i++)
+          for (int j = 0; j < n; j++) {
+            const double A = al[i] * al[j] - Ki[i * n + j];
+            if (i == j) tr += A;
+            se += A * Ex[i * n + j];
+            sed += A * Ex[i * n + j] * t->data[i * n + j];
+          }
+        g[0] = sigma * tr - x[0];
+        g[1] = tau * se - x[1];
+        g[2] = -lam * tau * tau * sed - x[2];
+      }
+      free(K);
+      if (t->residual) return lml;
+      return lml - 0.5 * ((x[0] * x[0] + x[1] * x[1]) + x[2] * x[2]) - 1.5 * LOG_2PI;
+    }
     case OR_T_BOX: { /* uniform on [p0, p1]^d */
       if (g)
         for (int k = 0; k < d; k++) g[k] = 0.0;
@@ -691,6 +768,7 @@ static int run_shared(chain* c, int* did) {
 typedef struct run_ctx {
   const or_kernel* k;
   const or_target* t;
+  or_target tcopy;   /* the caller's target with `residual` set for the kernel family */
   int64_t m, n, chain_offset;
   uint64_t seed;
   const double* x0;
@@ -875,7 +953,10 @@ static void ctx_setup(run_ctx* ctx, const or_kernel* k, const or_target* t, int6
                       or_run_out* out) {
   memset(ctx, 0, sizeof(*ctx));
   ctx->k = k;
-  ctx->t = t;
+  ctx->tcopy = *t;
+  ctx->tcopy.residual = k->family == OR_ESS; /* ESS evaluates the prior residual */
+  ctx->t = &ctx->tcopy;
+  t = ctx->t;
   ctx->m = m;
   ctx->n = n;
   ctx->seed = seed;

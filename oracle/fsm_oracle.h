@@ -30,14 +30,16 @@ enum {
   OR_T_LOGISTIC = 5,  /* -sum logaddexp(0, -y*x)  (GP-classification f-space) */
   OR_T_FLAT = 6,      /* log_density = 0 */
   OR_T_LOGREG = 7,    /* Bayesian logistic regression, N(0, I) prior (make_golden.py logreg_target) */
-  OR_T_BOX = 8        /* 0 on [p0, p1]^d, -inf outside (pkg/tests/test_kernels.py:205-212) */
+  OR_T_BOX = 8,       /* 0 on [p0, p1]^d, -inf outside (pkg/tests/test_kernels.py:205-212) */
+  OR_T_GP = 9         /* GP hyperparameters (sigma, tau, lam), targets.py:191-265; p0 = jitter,
+                         data = [n*n] squared distances, yvec = [n] outputs */
 };
 
 typedef struct or_target {
   int32_t kind;
   int32_t dim;
   int32_t n_modes;      /* MoG */
-  int32_t pad0;
+  int32_t residual;     /* GP: 1 = marginal likelihood only (the Gaussian-prior residual) */
   double log_norm;      /* gaussian / mog normaliser as the reference computes it */
   double p0, p1;        /* funnel: v_scale; nanband: threshold, value */
   const double* mean;   /* [d]           gaussian */

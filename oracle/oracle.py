@@ -28,7 +28,7 @@ LOG_2PI = math.log(2.0 * math.pi)
 
 DRMH, ESS, NUTS, SLICE = 1, 2, 3, 4
 VARIANTS = {"plain": 0, "bundled": 1, "amortized": 2}
-T_GAUSS, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, T_LOGREG, T_BOX = 1, 2, 3, 4, 5, 6, 7, 8
+T_GAUSS, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, T_LOGREG, T_BOX, T_GP = range(1, 10)
 
 
 def build(force: bool = False) -> str:
@@ -44,7 +44,7 @@ _PI64 = ctypes.POINTER(ctypes.c_int64)
 
 class _Target(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("dim", ctypes.c_int32), ("n_modes", ctypes.c_int32),
-                ("pad0", ctypes.c_int32), ("log_norm", ctypes.c_double),
+                ("residual", ctypes.c_int32), ("log_norm", ctypes.c_double),
                 ("p0", ctypes.c_double), ("p1", ctypes.c_double),
                 ("mean", _P), ("L_inv", _P), ("prec", _P), ("modes", _P), ("yvec", _P),
                 ("prior_chol", _P), ("prior_identity", ctypes.c_int32), ("pad1", ctypes.c_int32),
@@ -120,11 +120,13 @@ class OracleTarget:
     p1: float = 0.0
     arrays: dict = field(default_factory=dict)
     prior_identity: bool = False
+    residual: bool = False     # GP: evaluate the marginal likelihood only
 
     def struct(self) -> _Target:
         a = self.arrays
         t = _Target(kind=self.kind, dim=self.dim, n_modes=self.n_modes, log_norm=self.log_norm,
-                    p0=self.p0, p1=self.p1, prior_identity=int(self.prior_identity))
+                    p0=self.p0, p1=self.p1, prior_identity=int(self.prior_identity),
+                    residual=int(self.residual))
         for name in ("mean", "L_inv", "prec", "modes", "yvec", "prior_chol", "data"):
             if a.get(name) is not None:
                 setattr(t, name, _ptr(a[name]))
@@ -207,6 +209,22 @@ def logreg(X, y) -> OracleTarget:
     X = np.ascontiguousarray(np.asarray(X, dtype=float))
     y = np.ascontiguousarray(np.asarray(y, dtype=float))
     return OracleTarget(T_LOGREG, X.shape[1], arrays={"data": X, "yvec": y})
+
+
+def gp_hyper(X, y, jitter=1e-8) -> OracleTarget:
+    """GP hyperparameter posterior (targets.py:191-265); the squared distances are
+    formed exactly as the reference forms them, so C starts from the same matrix.
+    The elliptical kernel evaluates its marginal likelihood (identity prior)."""
+    X = np.asarray(X, dtype=float)
+    sq = np.sum(X * X, axis=1)
+    d2 = sq[:, None] + sq[None, :] - 2.0 * (X @ X.T)
+    np.maximum(d2, 0.0, out=d2)
+    t = OracleTarget(T_GP, 3, p0=float(jitter),
+                     arrays={"data": np.ascontiguousarray(d2),
+                             "yvec": np.ascontiguousarray(np.asarray(y, dtype=float))})
+    t.arrays["prior_chol"] = np.eye(3)
+    t.prior_identity = True
+    return t
 
 
 def with_prior(residual: OracleTarget, chol) -> OracleTarget:

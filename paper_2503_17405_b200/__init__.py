@@ -17,7 +17,9 @@ from .prng import RngKey, key, normal, normal_vec, split, uniform, uniform_block
 from .targets import (GaussianPriorDecomposition, TargetError, TargetModel, conjugate_target,
                       correlated_mog_target, equicorrelated_covariance,
                       box_target, equicorrelated_gaussian_target, funnel_target, gaussian_target,
-                      gp_classification_target, standard_normal_target)
+                      gp_classification_target, gp_hyperparameter_target,
+                      load_gp_dataset_csv, make_synthetic_gp_dataset, save_gp_dataset_csv,
+                      standard_normal_target)
 from .analysis import EssSummary, effective_sample_size, rhat
 
 __version__ = "0.1.0"

@@ -22,7 +22,7 @@ MAX_MODES = 8
 DRMH, ESS, NUTS, SLICE = 1, 2, 3, 4
 PLAIN, BUNDLED, AMORTIZED = 0, 1, 2
 T_GAUSS_DIAG, T_GAUSS_DENSE, T_GAUSS_EQUICORR, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, \
-    T_LOGREG, T_BOX = range(1, 11)
+    T_LOGREG, T_BOX, T_GP_HYPER = range(1, 12)
 PRIOR_NONE, PRIOR_IDENTITY, PRIOR_DENSE = 0, 1, 2
 
 # per-chain int slots
@@ -30,7 +30,7 @@ I_COUNTER, I_STREAM, I_STATE, I_TICK, I_COUNT = 0, 1, 2, 3, 4
 I_ERR_KIND, I_ERR_LABEL, I_ERR_TICK, I_ERR_ITER = 5, 6, 7, 8
 I_SHARED, I_BLOCKS, I_PEND, I_FAMILY, I_RESUME = 9, 10, 16, 20, 31
 SLICE_LABEL = 7   # device label of check_log_density(.., "slice")
-E_NONE, E_BLOCK, E_ZERO_START, E_GRAD, E_INIT = 0, 1, 2, 3, 4
+E_NONE, E_BLOCK, E_ZERO_START, E_GRAD, E_INIT, E_TARGET = 0, 1, 2, 3, 4, 5
 
 _D = ctypes.c_double
 _P = ctypes.c_void_p
@@ -54,7 +54,7 @@ class Kernel(ctypes.Structure):
 class Target(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("dim", ctypes.c_int32), ("n_modes", ctypes.c_int32),
                 ("prior_kind", ctypes.c_int32), ("log_norm", _D), ("a", _D), ("b", _D),
-                ("pad", _D), ("offsets", _D * MAX_MODES), ("mean", _P), ("diag", _P),
+                ("full", ctypes.c_int32), ("scratch", ctypes.c_int32), ("offsets", _D * MAX_MODES), ("mean", _P), ("diag", _P),
                 ("diag2", _P), ("mat_t", _P), ("mat2_t", _P), ("yvec", _P), ("prior_t", _P),
                 ("data", _P), ("n_rows", ctypes.c_int64)]
 

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) target_eval_kernel(fsmc_target t, co
                                                                long long m, double* lp, double* grad) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, t.dim);
+  double* sm = group_scratch<G, E>(smem, group_doubles(t));
   const int d = t.dim;
   const long long groups = (long long)gridDim.x * (kThreads / G);
   for (long long j = (long long)blockIdx.x * (kThreads / G) + threadIdx.x / G; j < m; j += groups) {
@@ -227,7 +227,11 @@ struct GE {
 
 // smallest compiled E for the requested lanes (auto: thread-per-chain for
 // small d, a warp per chain beyond)
-bool pick_config(int family, int dim, int lanes, GE& out) {
+// the per-chain GP plugin keeps two n x n matrices per chain in shared
+// memory (4 chains per block); larger designs use the batched evaluator
+constexpr int kGpMaxRows = 56;
+
+bool pick_config(int family, int dim, int lanes, GE& out, int kind = 0) {
   static const GE drmh[] = {
 #define X(GG, EE) {GG, EE},
       FSMC_DRMH_CONFIGS(X)};
@@ -245,7 +249,8 @@ bool pick_config(int family, int dim, int lanes, GE& out) {
             : family == FSMC_ESS ? (int)(sizeof(ess) / sizeof(GE))
                                  : (int)(sizeof(nuts) / sizeof(GE));
   if (lanes <= 0) {
-    if (family == FSMC_DRMH && dim <= 16) lanes = 1;
+    if (kind == FSMC_T_GP_HYPER) lanes = 32;   // a warp factors the chain's kernel matrix
+    else if (family == FSMC_DRMH && dim <= 16) lanes = 1;
     else if (dim <= 4) lanes = 1;
     else if (family == FSMC_NUTS && dim <= 16) lanes = 4;
     else if (family == FSMC_ESS && dim > 256) lanes = 128;
@@ -258,7 +263,7 @@ bool pick_config(int family, int dim, int lanes, GE& out) {
     if (c.g != lanes || c.g * c.e < dim) continue;
     if (!best || c.e < best->e) best = &c;
   }
-  if (!best && lanes == 1) return pick_config(family, dim, family == FSMC_NUTS && dim <= 16 ? 4 : 32, out);
+  if (!best && lanes == 1) return pick_config(family, dim, family == FSMC_NUTS && dim <= 16 ? 4 : 32, out, kind);
   if (!best) return false;
   out = *best;
   return true;
@@ -303,6 +308,10 @@ fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_st
     return fail(FSMC_ERR_ARG, "slice sampling here is univariate");
   if (k->family == FSMC_ESS && t->prior_kind == FSMC_PRIOR_NONE)
     return fail(FSMC_ERR_ARG, "elliptical slice sampling needs a Gaussian-prior split");
+  if (t->kind == FSMC_T_GP_HYPER &&
+      (t->dim != 3 || t->n_rows < 2 || t->n_rows > kGpMaxRows || !t->data || !t->yvec ||
+       t->scratch < 2 * t->n_rows * t->n_rows + 2 * t->n_rows + 4))
+    return fail(FSMC_ERR_ARG, "GP target: dim 3, 2 <= n <= 56 observations, scratch 2n^2+2n+4");
   if (t->kind == FSMC_T_MOG && (t->n_modes < 1 || t->n_modes > FSMC_MAX_MODES))
     return fail(FSMC_ERR_ARG, "n_modes out of range");
   return FSMC_OK;
@@ -350,10 +359,11 @@ fsmc_status fsmc_init(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   GE ge;
-  if (!pick_config(k->family, t->dim, 0, ge)) return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+  if (!pick_config(k->family, t->dim, 0, ge, t->kind)) return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
   Params p;
   memset(&p, 0, sizeof(p));
   p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = k->family != FSMC_ESS;
   cudaStream_t cs = (cudaStream_t)stream_;
   CUDA_TRY(cudaMemsetAsync(st->err_key, 0xff, sizeof(unsigned long long), cs));
   CUDA_TRY(dispatch_family(0, ge, p, cs, parent_stream, chain_offset, x0, init_jitter));
@@ -368,11 +378,12 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
   if (n < 0) return fail(FSMC_ERR_ARG, "n must be >= 0");
   if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
   GE ge;
-  if (!pick_config(k->family, t->dim, lanes, ge))
+  if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
     return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
   Params p;
   memset(&p, 0, sizeof(p));
   p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = k->family != FSMC_ESS;
   if (out) p.out = *out;
   p.n = n;
   p.tick_limit = tick_limit;
@@ -397,11 +408,12 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
     return fail(FSMC_ERR_ARG, "advance needs theta, req_chain, req_count, lp (and grad for NUTS)");
   if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
   GE ge;
-  if (!pick_config(k->family, t->dim, lanes, ge))
+  if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
     return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
   Params p;
   memset(&p, 0, sizeof(p));
   p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = k->family != FSMC_ESS;
   if (out) p.out = *out;
   p.n = n;
   p.tick_limit = tick_limit;
@@ -427,11 +439,12 @@ fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   GE ge;
-  if (!pick_config(k->family, t->dim, lanes, ge))
+  if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
     return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
   Params p;
   memset(&p, 0, sizeof(p));
   p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = k->family != FSMC_ESS;
   if (out) p.out = *out;
   p.n = n;
   cudaStream_t cs = (cudaStream_t)stream_;
@@ -449,14 +462,17 @@ fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, d
   if (!t || !X || !lp || m < 0) return fail(FSMC_ERR_ARG, "bad target_eval args");
   if (!m) return FSMC_OK;
   GE ge;
-  if (!pick_config(family ? family : FSMC_ESS, t->dim, lanes, ge))
+  if (!pick_config(family ? family : FSMC_ESS, t->dim, lanes, ge, t->kind))
     return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+  fsmc_target tt = *t;
+  tt.full = family != FSMC_ESS;   // 0 = the default layout, full log density
   cudaStream_t cs = (cudaStream_t)stream_;
   long long groups = (m + kThreads / ge.g - 1) / (kThreads / ge.g);
   int blocks = (int)std::min<long long>(groups, 148LL * 8);
 #define X(GG, EE)                                                                           \
   if (ge.g == GG && ge.e == EE) {                                                           \
-    target_eval_kernel<GG, EE><<<blocks, kThreads, smem_bytes<GG, EE>(t->dim), cs>>>(*t, X, m, lp, grad); \
+    CUDA_TRY(allow_smem(target_eval_kernel<GG, EE>, smem_bytes<GG, EE>(group_doubles(tt))));     \
+    target_eval_kernel<GG, EE><<<blocks, kThreads, smem_bytes<GG, EE>(group_doubles(tt)), cs>>>(tt, X, m, lp, grad); \
     CUDA_TRY(cudaGetLastError());                                                         \
     return FSMC_OK;                                                                       \
   }

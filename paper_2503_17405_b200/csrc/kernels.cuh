@@ -19,19 +19,27 @@ namespace fsmc {
 constexpr int kThreads = 128;
 
 // dynamic shared memory: one cooperative-normal scratch per warp, then the
-// per-group dense-operator scratch (dim doubles per lane group)
+// per-group plugin scratch (dim doubles for dense operators plus whatever
+// the plugin asks for in fsmc_target.scratch, e.g. a GP kernel matrix)
+__host__ __device__ inline int group_doubles(const fsmc_target& t) { return t.dim + t.scratch; }
 template <int G, int E>
-__device__ __forceinline__ double* warp_scratch(double* smem, int dim) {
+__device__ __forceinline__ double* warp_scratch(double* smem, int gd) {
   return smem + (threadIdx.x >> 5) * normal_scratch_doubles<E>();
 }
 template <int G, int E>
-__device__ __forceinline__ double* group_scratch(double* smem, int dim) {
-  return smem + (kThreads / 32) * normal_scratch_doubles<E>() + (threadIdx.x / G) * dim;
+__device__ __forceinline__ double* group_scratch(double* smem, int gd) {
+  return smem + (kThreads / 32) * normal_scratch_doubles<E>() + (threadIdx.x / G) * gd;
 }
 template <int G, int E>
-inline size_t smem_bytes(int dim) {
-  return ((size_t)(kThreads / G) * dim + (size_t)(kThreads / 32) * normal_scratch_doubles<E>()) *
+inline size_t smem_bytes(int gd) {
+  return ((size_t)(kThreads / G) * gd + (size_t)(kThreads / 32) * normal_scratch_doubles<E>()) *
          sizeof(double);
+}
+// opt a kernel into more than 48 KB of dynamic shared memory when needed
+template <class K>
+inline cudaError_t allow_smem(K* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 // registers: 4 resident blocks per SM for thread-per-chain configurations so
@@ -55,10 +63,10 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
   extern __shared__ double smem[];
   Grp<G> grp;
   const int gib = threadIdx.x / G;
-  double* sm = group_scratch<G, E>(smem, p.t.dim);
+  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
   const long long groups = (long long)gridDim.x * (kThreads / G);
   const int d = p.t.dim;
-  double* ws = warp_scratch<G, E>(smem, p.t.dim);
+  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
   for (long long j = (long long)blockIdx.x * (kThreads / G) + gib; j < p.st.m; j += groups) {
     Core c;
     memset(&c, 0, sizeof(c));
@@ -85,7 +93,12 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
     } else {
       f.init_pre();
       double lp = target_eval<G, E, false>(p.t, f.ev(), f.evg(), sm, grp);
-      ok = f.init_post(c, lp);
+      if (is_target_failure(lp)) {
+        set_error(c, FSMC_E_TARGET, 1);
+        ok = false;
+      } else {
+        ok = f.init_post(c, lp);
+      }
     }
     f.store(p, j, grp);
     if (grp.lane == 0) {
@@ -104,8 +117,8 @@ template <template <int, int> class F, int G, int E, int TK>
 __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, p.t.dim);
-  double* ws = warp_scratch<G, E>(smem, p.t.dim);
+  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
+  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
   while (true) {
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
@@ -137,8 +150,8 @@ template <template <int, int> class F, int G, int E>
 __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_advance_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, p.t.dim);
-  double* ws = warp_scratch<G, E>(smem, p.t.dim);
+  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
+  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
   while (true) {
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
@@ -198,15 +211,15 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
   using FF = F<G, E>;
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, p.t.dim);
+  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
   const long long j = p.wave_lo + (long long)blockIdx.x * (kThreads / G) + threadIdx.x / G;
   bool live = j < p.wave_hi;
   Core c;
-  c.ws = warp_scratch<G, E>(smem, p.t.dim);
+  c.ws = warp_scratch<G, E>(smem, group_doubles(p.t));
   FF f;
   if (live) {
     core_load(c, p, j);
-    c.ws = warp_scratch<G, E>(smem, p.t.dim);
+    c.ws = warp_scratch<G, E>(smem, group_doubles(p.t));
     f.load(p, j, grp);
     live = c.err_kind == FSMC_E_NONE;
   }
@@ -274,17 +287,21 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
 // ------------------------------------------------------------- launchers
 template <template <int, int> class F, int G, int E, int TK>
 struct Launch {
-  static size_t smem(const Params& p) { return smem_bytes<G, E>(p.t.dim); }
+  static size_t smem(const Params& p) { return smem_bytes<G, E>(group_doubles(p.t)); }
   static cudaError_t init(const Params& p, uint64_t ps, long long off, const double* x0, double jit,
                           cudaStream_t s) {
     long long groups = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
     int blocks = (int)std::min<long long>(groups, 1 << 20);
+    cudaError_t e = allow_smem(fsm_init_kernel<F, G, E>, smem(p));
+    if (e != cudaSuccess) return e;
     fsm_init_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p, ps, off, x0, jit);
     return cudaGetLastError();
   }
   static cudaError_t run(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_run_kernel<F, G, E, TK>,
+    cudaError_t e = allow_smem(fsm_run_kernel<F, G, E, TK>, smem(p));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_run_kernel<F, G, E, TK>,
                                                                   kThreads, smem(p));
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
@@ -295,7 +312,9 @@ struct Launch {
   }
   static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_advance_kernel<F, G, E>,
+    cudaError_t e = allow_smem(fsm_advance_kernel<F, G, E>, smem(p));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_advance_kernel<F, G, E>,
                                                                   kThreads, smem(p));
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
@@ -306,7 +325,9 @@ struct Launch {
   }
   static cudaError_t lockstep(Params p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lockstep_kernel<F, G, E, TK>,
+    cudaError_t e = allow_smem(lockstep_kernel<F, G, E, TK>, smem(p));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lockstep_kernel<F, G, E, TK>,
                                                                   kThreads, smem(p));
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorLaunchOutOfResources;

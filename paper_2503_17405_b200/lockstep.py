@@ -258,6 +258,9 @@ def _cause(bundle, kind: int, label: int) -> Exception:
         return KernelError("starting point has zero density")
     if kind == _lib.E_GRAD:
         return KernelError("non-finite gradient")
+    if kind == _lib.E_TARGET:   # targets.py:213-218
+        from .targets import TargetError
+        return TargetError("kernel matrix not positive definite even with jitter")
     if kind == _lib.E_INIT:     # the Locals constructor's check (e.g. drmh.py:45, slice_sampling.py:38)
         return BlockFailure(labels[0], "log-density evaluated to a non-finite value (NaN or +inf)")
     if label == _lib.SLICE_LABEL:

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import struct
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -66,6 +67,8 @@ class TargetModel:
     gaussian_prior: GaussianPriorDecomposition | None = None
     log_density_cost: float = 1.0
     has_gradient: bool = True
+    scratch: int = 0               # per-chain shared-memory doubles the plugin needs
+    residual_only: bool = False    # evaluates the Gaussian-prior residual, not the density
     _dev: dict = field(default_factory=dict, repr=False)
     _struct: object = field(default=None, repr=False)
 
@@ -95,6 +98,7 @@ class TargetModel:
         t.log_norm = self.log_norm
         t.a = self.a
         t.b = self.b
+        t.scratch = self.scratch
         for i, o in enumerate(self.offsets):
             t.offsets[i] = o
         for name in ("mean", "diag", "diag2", "mat_t", "mat2_t", "yvec", "data"):
@@ -121,20 +125,21 @@ class TargetModel:
         lp = torch.empty(m, dtype=torch.float64, device="cuda")
         g = torch.empty_like(X) if grad else None
         t = self.struct()
+        fam = _lib.ESS if self.residual_only else 0
         _lib.check(_lib.lib().fsmc_target_eval(ctypes.byref(t), X.data_ptr(), m, lp.data_ptr(),
-                                               _lib.ptr(g), 0, 0, _lib.stream_ptr()),
+                                               _lib.ptr(g), fam, 0, _lib.stream_ptr()),
                    "fsmc_target_eval")
         return lp, g
 
     def log_density(self, x) -> float:
-        return float(self._eval(x, False)[0][0].item())
+        return _checked(float(self._eval(x, False)[0][0].item()))
 
     def gradient(self, x) -> np.ndarray:
         return self._eval(x, True)[1][0].cpu().numpy()
 
     def log_density_and_grad(self, x):
         lp, g = self._eval(x, True)
-        return float(lp[0].item()), g[0].cpu().numpy()
+        return _checked(float(lp[0].item())), g[0].cpu().numpy()
 
     def log_density_batch(self, X: torch.Tensor, grad: bool = False):
         """Batched device evaluation over rows of X [m, dim]."""
@@ -142,6 +147,17 @@ class TargetModel:
 
     def residual(self) -> "TargetModel":
         return self if self.gaussian_prior is None else self.gaussian_prior.residual_log_density
+
+
+_TARGET_FAILURE_BITS = 0x7ff80000dead0001   # csrc/fsm_device.cuh target_failure()
+
+
+def _checked(v: float) -> float:
+    """Raise TargetError where the plugin could not evaluate (the reference's
+    TargetError, e.g. targets.py:213-218) instead of returning its NaN payload."""
+    if v != v and struct.unpack("<Q", struct.pack("<d", v))[0] == _TARGET_FAILURE_BITS:
+        raise TargetError("kernel matrix not positive definite even with jitter")
+    return v
 
 
 def _check_chol(L, name="covariance factor") -> np.ndarray:
@@ -299,6 +315,72 @@ def conjugate_target(dim=2, rho=0.3, lik_mu=0.5, lik_var=0.5) -> TargetModel:
     prior_cov = equicorrelated_covariance(dim, rho)
     lik = gaussian_target(np.full(dim, lik_mu), np.linalg.cholesky(lik_var * np.eye(dim)))
     return _with_prior(lik, np.linalg.cholesky(prior_cov), "conjugate")
+
+
+# ------------------------------------------------------- GP hyperparameters
+GP_DATA_SEED = 20240617
+GP_DATA_THETA = (0.3, 1.0, 1.0)
+GP_DEVICE_MAX_ROWS = 56     # per-chain plugin limit (two n x n matrices in shared memory)
+
+
+def _sq_dists(X: np.ndarray) -> np.ndarray:
+    """||x_i - x_j||^2 exactly as targets.py:206-209 forms it (so the device
+    reads the reference's own distance matrix)."""
+    sq = np.sum(X * X, axis=1)
+    d2 = sq[:, None] + sq[None, :] - 2.0 * (X @ X.T)
+    np.maximum(d2, 0.0, out=d2)
+    return d2
+
+
+def gp_hyperparameter_target(inputs, outputs, jitter: float = 1e-8) -> TargetModel:
+    """Posterior over theta = (sigma, tau, lam) of a squared-exponential GP
+    regression (targets.py:191-265): K = tau^2 exp(-lam^2 D2) + (sigma^2 +
+    jitter) I, N(0, 1) priors, so the Gaussian-prior split has the identity
+    factor and the marginal likelihood as residual.  Each evaluation factors
+    the chain's own n x n kernel matrix in shared memory (one warp per chain);
+    the gradient adds W = L^-1 and the three trace terms."""
+    X = np.asarray(inputs, dtype=float)
+    y = np.ascontiguousarray(np.asarray(outputs, dtype=float))
+    if X.ndim != 2 or X.shape[0] < 2:
+        raise TargetError("inputs must be an n x p matrix with n >= 2")
+    if y.shape != (X.shape[0],):
+        raise TargetError(f"outputs shape {y.shape} does not match {X.shape[0]} rows")
+    n = X.shape[0]
+    if n > GP_DEVICE_MAX_ROWS:
+        raise TargetError(f"the per-chain GP plugin handles n <= {GP_DEVICE_MAX_ROWS} "
+                          f"observations, got {n}")
+    arrays = {"data": np.ascontiguousarray(_sq_dists(X)), "yvec": y}
+    common = dict(name=f"gp-hyper-n{n}", dim=3, kind=_lib.T_GP_HYPER, a=float(jitter),
+                  arrays=arrays, scratch=2 * n * n + 2 * n + 4,
+                  log_density_cost=(n / 50.0) ** 3)
+    residual = TargetModel(**common, residual_only=True)
+    return TargetModel(**common, gaussian_prior=GaussianPriorDecomposition(np.eye(3), residual))
+
+
+def make_synthetic_gp_dataset(n: int = 50, p: int = 3, seed: int = GP_DATA_SEED,
+                              theta=GP_DATA_THETA):
+    """(inputs, outputs) drawn from the GP model at fixed hyperparameters
+    (targets.py:273-287; same numpy draws, so the same data)."""
+    if n < 2:
+        raise TargetError("need n >= 2 data points")
+    sigma, tau, lam = theta
+    rng = np.random.default_rng(seed)
+    X = rng.normal(size=(n, p))
+    Kf = (tau * tau) * np.exp(-(lam * lam) * _sq_dists(X)) + 1e-10 * np.eye(n)
+    f = np.linalg.cholesky(Kf) @ rng.normal(size=n)
+    return X, f + sigma * rng.normal(size=n)
+
+
+def save_gp_dataset_csv(path, X, y) -> None:
+    """Feature columns then the output, one header line (targets.py:290-294)."""
+    X = np.asarray(X, dtype=float)
+    header = ",".join([f"x{i}" for i in range(X.shape[1])] + ["y"])
+    np.savetxt(path, np.column_stack([X, y]), delimiter=",", header=header, comments="")
+
+
+def load_gp_dataset_csv(path):
+    data = np.loadtxt(path, delimiter=",", skiprows=1)
+    return data[:, :-1], data[:, -1]
 
 
 def logistic_regression_data(n_obs: int = 100_000, d: int = 256, seed: int = 0):

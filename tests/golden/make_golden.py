@@ -30,7 +30,8 @@ from fsm_mcmc.lockstep import (KernelRunError, TickBudgetExceeded,  # noqa: E402
                                init_batch, run_fsm_batched, run_standard_batched)
 from fsm_mcmc.targets import (GaussianPriorDecomposition, TargetModel,  # noqa: E402
                               correlated_mog_target, equicorrelated_covariance,
-                              gaussian_target)
+                              gaussian_target, gp_hyperparameter_target,
+                              make_synthetic_gp_dataset)
 from tests_common_conjugate import conjugate_target  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -249,6 +250,7 @@ def main():
     main_split_only()
     main_slice_only()
     main_efficiency_only()
+    main_gp_only()
 
 
 def main_split_only():
@@ -297,6 +299,21 @@ def main_slice_only():
     print("wrote errors_slice", out)
 
 
+def main_gp_only():
+    """The GP-hyperparameter posterior (targets.py:191-265; the paper's section
+    7.2 workload) under all three multivariate kernels."""
+    X, y = make_synthetic_gp_dataset(50, 3)
+    t = gp_hyperparameter_target(X, y)
+    ex = {"X": X, "y": y}
+    x0 = np.array([0.3, 1.0, 1.0])
+    run_case("ess_gp50", elliptical_kernel(), t, m=6, n=60, seed=13,
+             variants=("amortized", "bundled"), extra=ex, x0=x0)
+    run_case("drmh_gp50", drmh_kernel(20, 0.2), t, m=6, n=60, seed=14,
+             variants=("plain", "bundled"), extra=ex, x0=x0)
+    run_case("nuts_gp50", nuts_kernel(0.1, 6), t, m=4, n=25, seed=15,
+             variants=("plain", "bundled"), extra=ex, x0=x0)
+
+
 def main_efficiency_only():
     """Cost-theory analytics (analysis.py:53-324) on fixed inputs."""
     from fsm_mcmc import analysis as A
@@ -341,5 +358,7 @@ if __name__ == "__main__":
         main_slice_only()
     elif len(sys.argv) > 1 and sys.argv[1] == "efficiency":
         main_efficiency_only()
+    elif len(sys.argv) > 1 and sys.argv[1] == "gp":
+        main_gp_only()
     else:
         main()

@@ -37,7 +37,19 @@ CASES = {
     "slice_narrow": (("plain", "bundled", "standard"), ("slice", 0.2, 50), ("gauss", np.array([1.5]), np.array([[2.0]]))),
     "slice_cap": (("plain", "bundled", "standard"), ("slice", 0.05, 3), ("gauss", np.zeros(1), np.eye(1))),
     "slice_box": (("plain", "bundled", "standard"), ("slice", 10.0, 8), ("box", 1, 0.0, 1.0)),
+    "ess_gp50": (("amortized", "bundled", "standard"), ("ess",), ("gphyper", "ess_gp50")),
+    "drmh_gp50": (("plain", "bundled", "standard"), ("drmh", 20, 0.2), ("gphyper", "drmh_gp50")),
+    "nuts_gp50": (("plain", "bundled", "standard"), ("nuts", 0.1, 6, 1000.0), ("gphyper", "nuts_gp50")),
 }
+
+# sample tolerance per case (relative, |a-b| <= tol max(1, |b|)): 1e-12 by default; the
+# GP cases factor a 50 x 50 kernel matrix whose LAPACK (OpenBLAS) operation order is
+# not restated, and cond(K) ~ 1e3 amplifies the last-ulp differences
+SAMPLE_TOL = {"ess_gp50": 1e-9, "drmh_gp50": 1e-9, "nuts_gp50": 1e-9}
+
+
+def sample_tol(name):
+    return SAMPLE_TOL.get(name, 1e-12)
 
 # cases the oracle does not restate (checked against the goldens on the device only)
 DEVICE_ONLY = {"drmh_split_std1", "drmh_split_mog10"}
@@ -68,6 +80,9 @@ def oracle_target(spec):
         return O.funnel(spec[1])
     if kind == "box":
         return O.box(spec[1], spec[2], spec[3])
+    if kind == "gphyper":
+        g = load(spec[1])
+        return O.gp_hyper(g["X"], g["y"])
     if kind == "gauss":
         return O.gaussian(spec[1], spec[2])
     if kind == "equicorr":
@@ -106,6 +121,9 @@ def device_target(spec, structure="auto"):
         return fm.funnel_target(spec[1])
     if kind == "box":
         return fm.box_target(spec[1], spec[2], spec[3])
+    if kind == "gphyper":
+        g = load(spec[1])
+        return fm.gp_hyperparameter_target(g["X"], g["y"])
     if kind == "gauss":
         return fm.gaussian_target(spec[1], spec[2], structure=structure)
     if kind == "equicorr":

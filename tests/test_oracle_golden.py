@@ -8,7 +8,7 @@ import math
 import numpy as np
 import pytest
 
-from golden_cases import CASES, DEVICE_ONLY, load, oracle_kernel, oracle_target, rel_err, x0_of
+from golden_cases import CASES, DEVICE_ONLY, load, oracle_kernel, oracle_target, rel_err, sample_tol, x0_of
 from oracle import oracle as O
 
 SAMPLE_TOL = 1e-12
@@ -58,7 +58,7 @@ def test_oracle_matches_reference(name):
         if v != "standard":
             assert np.array_equal(r["sample_ticks"], g[v + "_sample_ticks"]), v
             assert r["native_shared_evals"] == int(g[v + "_native_shared_evals"]), v
-        assert rel_err(r["samples"], g[v + "_samples"]) <= SAMPLE_TOL, v
+        assert rel_err(r["samples"], g[v + "_samples"]) <= sample_tol(name), v
 
 
 def test_oracle_errors_match_reference():
