@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define FSMC_ABI_VERSION 1
+#define FSMC_ABI_VERSION 2
 #define FSMC_NINT 32        /* int64 slots per chain in fsmc_state.ints */
 #define FSMC_MAX_MODES 8    /* mixture components in FSMC_T_MOG */
 
@@ -167,6 +167,16 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
  * waves, each with its own barriers. */
 fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                               int64_t n, const fsmc_outputs* out, int32_t lanes, void* stream_);
+
+/* Replaces measure_block_costs' timing loop (lockstep.py:454-498): runs every
+ * chain with the plain executor up to tick_limit like fsmc_run (mode 1) and
+ * adds per-state clock64() cycles to cycles[16] (device, zeroed by the
+ * caller): cycles[s-1] = state s's blocks excluding log-density evaluations,
+ * cycles[8+s-1] = the evaluations requested in state s.  Chains run one per
+ * warp where that layout is compiled, so divergent neighbours do not
+ * inflate a chain's clock deltas. */
+fsmc_status fsmc_profile_blocks(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                                int64_t tick_limit, unsigned long long* cycles, void* stream_);
 
 /* Batched plugin evaluation: lp[j] = log p(X[j]), grad[j] (if non-NULL) for
  * rows X[m][dim] (TargetModel.log_density / log_density_and_grad).  family /

@@ -12,7 +12,8 @@ from .fsm import (BlockFailure, FsmDefinition, FsmError, SharedComputation, Step
 from .kernels import KERNEL_BUILDERS, KernelBundle, KernelError, drmh_kernel, elliptical_kernel, \
     nuts_kernel, slice_kernel
 from .lockstep import (ChainBatch, CostLedger, CostParams, KernelRunError, TickBudgetExceeded,
-                       collect_samples, init_batch, run_fsm_batched, run_standard_batched)
+                       collect_samples, init_batch, measure_block_costs, run_fsm_batched,
+                       run_standard_batched)
 from .prng import RngKey, key, normal, normal_vec, split, uniform, uniform_block
 from .targets import (GaussianPriorDecomposition, TargetError, TargetModel, conjugate_target,
                       correlated_mog_target, equicorrelated_covariance,

@@ -15,6 +15,7 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FSMC_LIB", os.path.join(HERE, "libfsmc.so"))
 
+ABI_VERSION = 2    # fsmc.h FSMC_ABI_VERSION
 FSMC_NINT = 32
 MAX_MODES = 8
 
@@ -110,6 +111,9 @@ def lib():
     L.fsmc_lockstep_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                     ctypes.POINTER(State), ctypes.c_int64,
                                     ctypes.POINTER(Outputs), ctypes.c_int32, _P]
+    L.fsmc_profile_blocks.restype = S
+    L.fsmc_profile_blocks.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
+                                      ctypes.POINTER(State), ctypes.c_int64, _P, _P]
     L.fsmc_target_eval.restype = S
     L.fsmc_target_eval.argtypes = [ctypes.POINTER(Target), _P, ctypes.c_int64, _P, _P,
                                    ctypes.c_int32, ctypes.c_int32, _P]
@@ -122,7 +126,7 @@ def lib():
     L.fsmc_diag_partials.restype = S
     L.fsmc_diag_partials.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P]
-    if L.fsmc_abi_version() != 1:
+    if L.fsmc_abi_version() != ABI_VERSION:
         raise EngineUnavailable("libfsmc.so ABI version mismatch")
     _lib = L
     return L

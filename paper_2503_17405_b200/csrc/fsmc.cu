@@ -434,6 +434,32 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
   return FSMC_OK;
 }
 
+fsmc_status fsmc_profile_blocks(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                                int64_t tick_limit, unsigned long long* cycles, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (!cycles || tick_limit < 0) return fail(FSMC_ERR_ARG, "profile needs cycles[16] and tick_limit >= 0");
+  // one chain per warp where compiled: a lane group then never waits on
+  // other chains' divergent blocks, so its clock deltas are its own blocks
+  GE ge;
+  if (!pick_config(k->family, t->dim, 32, ge, t->kind) && !pick_config(k->family, t->dim, 0, ge, t->kind))
+    return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = k->family != FSMC_ESS;
+  p.n = 0;
+  p.tick_limit = tick_limit;
+  p.variant = FSMC_PLAIN;
+  p.mode = 1;
+  p.prof = cycles;
+  cudaStream_t cs = (cudaStream_t)stream_;
+  p.next_chain = scratch().words;
+  CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
+  CUDA_TRY(dispatch_family(4, ge, p, cs));
+  return FSMC_OK;
+}
+
 fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                               const fsmc_outputs* out, int32_t lanes, void* stream_) {
   fsmc_status s = check_args(k, t, st);

@@ -143,6 +143,39 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Para
   }
 }
 
+// ------------------------------------------------------------- profile
+// fsm_run_kernel with clock64() timing around every block and evaluation
+// (measure_block_costs, lockstep.py:454-498): the same ticks, the same
+// draws; only the per-state cycle totals in p.prof are extra.
+template <template <int, int> class F, int G, int E>
+__global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_profile_kernel(Params p) {
+  extern __shared__ double smem[];
+  Grp<G> grp;
+  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
+  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
+  while (true) {
+    long long j = 0;
+    if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
+    j = grp.bcast_ll(j, 0);
+    if (j >= p.st.m) break;
+    Core c;
+    core_load(c, p, j);
+    c.ws = ws;
+    if (c.err_kind != FSMC_E_NONE) continue;
+    F<G, E> f;
+    f.load(p, j, grp);
+    bool ok = true;
+#pragma unroll 1
+    while (c.tick < p.tick_limit)
+      if (!tick<F<G, E>, G, E, 0, true>(p, c, f, sm, j, grp, p.prof)) { ok = false; break; }
+    f.store(p, j, grp);
+    if (grp.lane == 0) {
+      core_store(c, p, j);
+      if (!ok) report_error(c, p, j);
+    }
+  }
+}
+
 // ------------------------------------------------------------- advance
 // Batched-evaluation mode: every chain runs to its next log-density request
 // and parks the point in the compact request list (see fsmc_advance).
@@ -310,6 +343,18 @@ struct Launch {
     fsm_run_kernel<F, G, E, TK><<<blocks, kThreads, smem(p), s>>>(p);
     return cudaGetLastError();
   }
+  static cudaError_t profile(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
+    int occ = 0;
+    cudaError_t e = allow_smem(fsm_profile_kernel<F, G, E>, smem(p));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_profile_kernel<F, G, E>, kThreads, smem(p));
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
+    int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
+    fsm_profile_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p);
+    return cudaGetLastError();
+  }
   static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
     cudaError_t e = allow_smem(fsm_advance_kernel<F, G, E>, smem(p));
@@ -346,13 +391,14 @@ struct Launch {
   }
 };
 
-// op: 0 init, 1 run, 2 lock-step.  TK: compile-time plugin (0 = run-time switch)
+// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile.  TK: compile-time plugin (0 = run-time switch)
 template <template <int, int> class F, int G, int E, int TK = 0>
 cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, uint64_t ps,
                       long long off, const double* x0, double jit) {
   if (op == 0) return Launch<F, G, E, 0>::init(p, ps, off, x0, jit, s);
   if (op == 1) return Launch<F, G, E, TK>::run(p, lc, s);
   if (op == 3) return Launch<F, G, E, 0>::advance(p, lc, s);
+  if (op == 4) return Launch<F, G, E, 0>::profile(p, lc, s);
   return Launch<F, G, E, TK>::lockstep(p, lc, s);
 }
 

@@ -32,6 +32,7 @@ from .prng import RngKey
 
 __all__ = ["ChainBatch", "CostParams", "CostLedger", "KernelRunError", "TickBudgetExceeded",
            "init_batch", "run_standard_batched", "run_fsm_batched", "collect_samples",
+           "measure_block_costs",
            "STEP_VARIANTS", "TICK_CHUNK"]
 
 STEP_VARIANTS = ("plain", "bundled", "amortized")
@@ -550,6 +551,52 @@ def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
                         tick_count=n, block_exec_counts=_convert(blocks, output),
                         charged_cost=charged, walltime=walltime, regime="standard")
     return _convert(samples, output), ledger
+
+
+def measure_block_costs(bundle, target, m: int = 8, seed: int = 0, ticks: int = 200) -> CostParams:
+    """Per-block costs from the device's own clock (lockstep.py:454-498).
+
+    One ``fsmc_profile_blocks`` launch runs ``ticks`` plain ticks of m fresh
+    chains with clock64() around every block and every log-density
+    evaluation.  The launch's wall time (CUDA events) is apportioned to the
+    states by their cycle shares, so a cost is the seconds of batch time one
+    execution accounts for at this occupancy.  With a shared computation the
+    evaluations are priced separately (``shared_cost``), as the reference
+    times ``shared.fn``; otherwise they stay inside their block.  Measured
+    costs vary run to run, as the reference's do."""
+    batch = init_batch(bundle, target, m, seed)
+    machine = bundle.fsm
+    K = machine.n_states
+    cycles = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    _lib.check(_lib.lib().fsmc_profile_blocks(ctypes.byref(batch.kernel),
+                                              ctypes.byref(target.struct()),
+                                              ctypes.byref(batch.struct()), int(ticks),
+                                              cycles.data_ptr(), _lib.stream_ptr()),
+               "fsmc_profile_blocks")
+    ev[1].record()
+    torch.cuda.synchronize()
+    batch._ran = True
+    err = batch.first_error()
+    if err is not None:
+        raise KernelRunError(chain=err[0], iteration=err[4], cause=_cause(bundle, err[1], err[2]))
+    seconds = ev[0].elapsed_time(ev[1]) / 1e3
+    cyc = [int(v) & ((1 << 64) - 1) for v in cycles.cpu().tolist()]
+    blk, evc = cyc[:K], cyc[8:8 + K]
+    counts = batch.ints[:, _lib.I_BLOCKS:_lib.I_BLOCKS + K].sum(0).tolist()
+    shared_evals = int(batch.ints[:, _lib.I_SHARED].sum())
+    per_cycle = seconds / max(1, sum(blk) + sum(evc))
+    if machine.shared is not None:
+        block_costs = tuple(blk[k] * per_cycle / counts[k] if counts[k] else 0.0 for k in range(K))
+        shared_cost = sum(evc) * per_cycle / shared_evals if shared_evals else 0.0
+        sites = tuple(machine.shared.sites.get(s, 0) for s in range(1, K + 1))
+    else:
+        block_costs = tuple((blk[k] + evc[k]) * per_cycle / counts[k] if counts[k] else 0.0
+                            for k in range(K))
+        shared_cost, sites = 0.0, (0,) * K
+    return CostParams(block_costs=block_costs, alpha=1.0, loop_states=tuple(sorted(machine.loop_states)),
+                      shared_cost=shared_cost, shared_sites=sites)
 
 
 def collect_samples(buffers: Sequence[Sequence], flags=None, n: int | None = None) -> list:

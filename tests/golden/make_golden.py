@@ -251,6 +251,7 @@ def main():
     main_slice_only()
     main_efficiency_only()
     main_gp_only()
+    main_cli_only()
 
 
 def main_split_only():
@@ -314,6 +315,41 @@ def main_gp_only():
              variants=("plain", "bundled"), extra=ex, x0=x0)
 
 
+CLI_CONFIGS = [
+    dict(kernel="drmh", target="std-normal", dim=2, chains=16, samples=200, variant="bundled",
+         seeds=(0, 1)),
+    dict(kernel="slice", target="std-normal", dim=1, chains=8, samples=150, variant="plain",
+         seeds=(3,)),
+    dict(kernel="nuts", target="gaussian-corr", dim=5, chains=6, samples=60, variant="bundled",
+         target_rho=0.9, seeds=(2,)),
+    dict(kernel="elliptical", target="gp-synthetic", chains=4, samples=40, variant="amortized",
+         seeds=(5,)),
+    dict(kernel="drmh", target="mog", dim=4, chains=12, samples=100, variant="plain",
+         drmh_split_body=True, target_rho=0.5, seeds=(7,)),
+]
+
+
+def main_cli_only():
+    """cli.py run_experiment rows (write=False) and config validation/hashes."""
+    import json
+    from fsm_mcmc import cli
+    out = {"runs": [], "validate": [], "hash_default": cli.RunConfig().config_hash()}
+    for kw in CLI_CONFIGS:
+        res = cli.run_experiment(cli.RunConfig(**kw), write=False)
+        out["runs"].append({"config": {k: list(v) if isinstance(v, tuple) else v
+                                       for k, v in kw.items()},
+                            "hash": res.config.config_hash(), "rows": res.rows})
+    for kw in (dict(kernel="slice", target="std-normal", dim=3), dict(kernel="elliptical"),
+               dict(kernel="bogus", chains=0, samples=0, variant="x", seeds=()),
+               dict(target="mog", target_rho=1.5, tick_budget=0, dim=0),
+               dict(kernel="nuts", nuts_step_size=-1.0, nuts_max_depth=0),
+               dict(kernel="drmh", drmh_max_tries=0, drmh_proposal_scale=0.0)):
+        out["validate"].append({"config": kw, "errors": cli.RunConfig(**kw).validate()})
+    with open(os.path.join(OUT, "cli.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote cli")
+
+
 def main_efficiency_only():
     """Cost-theory analytics (analysis.py:53-324) on fixed inputs."""
     from fsm_mcmc import analysis as A
@@ -360,5 +396,7 @@ if __name__ == "__main__":
         main_efficiency_only()
     elif len(sys.argv) > 1 and sys.argv[1] == "gp":
         main_gp_only()
+    elif len(sys.argv) > 1 and sys.argv[1] == "cli":
+        main_cli_only()
     else:
         main()
