@@ -26,3 +26,7 @@ oracle:
 clean:
 	rm -rf $(LIB) $(BUILD) oracle/liboracle.so
 .PHONY: all oracle clean
+
+# measured pipe ceilings (fp64 FMA, 64-bit multiply) for the compute roofline
+tools/peak_probe: tools/peak_probe.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<

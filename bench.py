@@ -28,6 +28,10 @@ import time
 
 import numpy as np
 
+# large per-step outputs (samples [n][m][d]) are reallocated every step: keep
+# the caching allocator from fragmenting into fresh cudaMalloc/cudaFree calls
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -36,7 +40,7 @@ METRIC = "samples/sec & ESS/sec at m chains (1/2/4/8 B200); speed-up vs lock-ste
 CONFIGS = {
     "c2": dict(workload="C2: DRMH FSM, correlated MoG d=10 (rho=0.9, modes -3/0/3), M=100, "
                         "scale=0.1, bundled", family="drmh", m=65536, n=1000, d=10,
-               variant="bundled", m_cpu=256),
+               variant="bundled", m_cpu=256, draw_window=2200),
     "c1": dict(workload="C1: elliptical slice FSM, conjugate Gaussian-likelihood d=100, amortized",
                family="ess", m=128, n=1000, d=100, variant="amortized", m_cpu=32),
     "c3": dict(workload="C3: NUTS FSM, equicorrelated Gaussian d=100 rho=0.99, eps=0.05, depth 10",
@@ -179,12 +183,16 @@ def main():
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--no-lockstep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--draw-window", type=int, default=-1,
+                    help="DRMH pre-drawn window in draws (0: inline generator; -1: config default)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.m:
         cfg["m"] = args.m
     if args.n:
         cfg["n"] = args.n
+    if args.draw_window >= 0:
+        cfg["draw_window"] = args.draw_window
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -229,10 +237,14 @@ def main():
         batch = fm.init_batch(bundle, target, m, seed, chain_offset=off)
         return fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
                                   output="torch", surplus=False, lanes=args.lanes,
-                                  evaluator=evaluator, _timing=timing)
+                                  evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
+                                  _timing=timing)
 
+    held = None
     for s in range(args.warmup):
-        one_step(1000 + s)
+        # keep the previous step's outputs alive exactly as the timed loop
+        # does, so the allocator holds both sample buffers before timing
+        held = one_step(1000 + s)
     barrier()
     clocks = ClockSampler(local)
     step_ms, kern_ms = [], []
@@ -248,6 +260,7 @@ def main():
         barrier()
         step_ms.append(e0.elapsed_time(e1))
         kern_ms.append(timing["run_kernel_ms"])
+        held = None
     clk = clocks.stop()
     t_total = max_over_ranks(sum(step_ms) / 1e3)
     value = world * m * n * args.steps / t_total
@@ -297,7 +310,7 @@ def main():
         batch = fm.init_batch(bundle, target, m, 500 + s, x0=x0, chain_offset=off)
         smp, _ = fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
                                     output="torch", surplus=False, lanes=args.lanes,
-                                    evaluator=evaluator)
+                                    evaluator=evaluator, draw_window=cfg.get("draw_window", 0))
         if has_ess:
             _ = fm.effective_sample_size(smp, burn=burn).pooled
         else:
@@ -357,7 +370,8 @@ def main():
                 "lockstep": lock, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
                 "clocks": clk, "gpu_launches": args.steps * (2 + (ledger.extras.get("rounds") or 0)),
                 "tick_count": ledger.tick_count,
-                "evaluations_per_step": evals, "rounds_per_step": ledger.extras.get("rounds")}
+                "evaluations_per_step": evals, "rounds_per_step": ledger.extras.get("rounds"),
+                "step_ms": [round(v, 3) for v in step_ms], "kernel_ms": [round(v, 3) for v in kern_ms]}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

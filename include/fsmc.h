@@ -124,7 +124,8 @@ enum {
   FSMC_I_COUNTER = 0, FSMC_I_STREAM = 1, FSMC_I_STATE = 2, FSMC_I_TICK = 3, FSMC_I_COUNT = 4,
   FSMC_I_ERR_KIND = 5, FSMC_I_ERR_LABEL = 6, FSMC_I_ERR_TICK = 7, FSMC_I_ERR_ITER = 8,
   FSMC_I_SHARED = 9, FSMC_I_BLOCKS = 10 /* 6 slots */, FSMC_I_PEND = 16 /* 4 slots */,
-  FSMC_I_FAMILY = 20 /* family-private slots 20..30 */,
+  FSMC_I_FAMILY = 20 /* family-private slots 20..29 */,
+  FSMC_I_DRAW0 = 30 /* counter at the end of init (draw-pattern origin) */,
   FSMC_I_RESUME = 31 /* batched mode: suspended-at-evaluation record */
 };
 /* error kinds in FSMC_I_ERR_KIND */
@@ -167,6 +168,22 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
  * waves, each with its own barriers. */
 fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                               int64_t n, const fsmc_outputs* out, int32_t lanes, void* stream_);
+
+/* fsmc_run for the DRMH kernels (drmh_kernel, split or not) with the draws
+ * generated ahead of use.  Every DRMH proposal consumes dim normals then one
+ * uniform (drmh.py:85-88), so a chain's draws from its current counter on are
+ * known before it runs.  Rounds alternate two kernels until every chain is
+ * done: a generator fills each unfinished chain's next `window` draws into
+ * draws [m][window] (full occupancy, every lane busy), then the step kernel
+ * runs each chain from its window until a tick could need more draws than
+ * remain.  Samples, ledgers, ticks and errors are identical to fsmc_run's.
+ * window >= dim + 1; `draws` holds m*window doubles plus 32 of slack (the step
+ * kernel prefetches one proposal ahead).  Synchronises the stream every few
+ * rounds (it reads the unfinished-chain count). */
+fsmc_status fsmc_run_windowed(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                              int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                              const fsmc_outputs* out, int64_t window, double* draws, int32_t lanes,
+                              void* stream_);
 
 /* Replaces measure_block_costs' timing loop (lockstep.py:454-498): runs every
  * chain with the plain executor up to tick_limit like fsmc_run (mode 1) and

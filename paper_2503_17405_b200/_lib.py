@@ -29,7 +29,7 @@ PRIOR_NONE, PRIOR_IDENTITY, PRIOR_DENSE = 0, 1, 2
 # per-chain int slots
 I_COUNTER, I_STREAM, I_STATE, I_TICK, I_COUNT = 0, 1, 2, 3, 4
 I_ERR_KIND, I_ERR_LABEL, I_ERR_TICK, I_ERR_ITER = 5, 6, 7, 8
-I_SHARED, I_BLOCKS, I_PEND, I_FAMILY, I_RESUME = 9, 10, 16, 20, 31
+I_SHARED, I_BLOCKS, I_PEND, I_FAMILY, I_DRAW0, I_RESUME = 9, 10, 16, 20, 30, 31
 SLICE_LABEL = 7   # device label of check_log_density(.., "slice")
 E_NONE, E_BLOCK, E_ZERO_START, E_GRAD, E_INIT, E_TARGET = 0, 1, 2, 3, 4, 5
 
@@ -111,6 +111,11 @@ def lib():
     L.fsmc_lockstep_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                     ctypes.POINTER(State), ctypes.c_int64,
                                     ctypes.POINTER(Outputs), ctypes.c_int32, _P]
+    L.fsmc_run_windowed.restype = S
+    L.fsmc_run_windowed.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
+                                    ctypes.POINTER(State), ctypes.c_int64, ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, ctypes.c_int32,
+                                    ctypes.POINTER(Outputs), ctypes.c_int64, _P, ctypes.c_int32, _P]
     L.fsmc_profile_blocks.restype = S
     L.fsmc_profile_blocks.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                       ctypes.POINTER(State), ctypes.c_int64, _P, _P]

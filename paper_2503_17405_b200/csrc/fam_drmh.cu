@@ -2,9 +2,99 @@
 #include "kernels.cuh"
 
 namespace fsmc {
+
+// The DRMH draw pattern (drmh.py:85-88): from the chain's draw origin on,
+// every group of dim + 1 counters is dim normals then one uniform.  One warp
+// fills one chain's window at a time (coalesced 256 B stores): uniforms and
+// central-branch normals directly, tail-branch normals through a per-warp
+// queue evaluated with every lane busy (the compaction of normal_vec).
+constexpr int kDrawChunk = 256;   // window slots per warp pass (tail-queue capacity)
+__global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
+  __shared__ double qy_all[8][kDrawChunk];
+  __shared__ unsigned qk_all[8][kDrawChunk];
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = (int)p.window, d = p.t.dim, per = d + 1;
+  double* qy = qy_all[wid];
+  unsigned* qk = qk_all[wid];
+  const unsigned lt = (1u << lane) - 1u;
+  const int step = 32 % per;             // phase advance between a lane's slots
+  const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
+  for (long long j = (long long)blockIdx.x * nw + wid; j < p.st.m; j += (long long)gridDim.x * nw) {
+    const int64_t* q = p.st.ints + (size_t)j * FSMC_NINT;
+    if (q[FSMC_I_ERR_KIND] != FSMC_E_NONE || q[FSMC_I_COUNT] >= n_stop || q[FSMC_I_TICK] >= p.tick_limit)
+      continue;
+    const uint64_t ctr0 = (uint64_t)q[FSMC_I_COUNTER];
+    const uint64_t hsc = hash_seed_stream(p.st.seed, (uint64_t)q[FSMC_I_STREAM]);
+    int phase = (int)((ctr0 - (uint64_t)q[FSMC_I_DRAW0]) % (uint64_t)per) + lane % per;
+    if (phase >= per) phase -= per;
+    double* out = p.draws + (size_t)j * W;
+    for (int c0 = 0; c0 < W; c0 += kDrawChunk) {
+      const int c1 = min(W, c0 + kDrawChunk);
+      int nt = 0;
+      for (int k0 = c0; k0 < c1; k0 += 32) {
+        const int k = k0 + lane;
+        bool tail = false, neg = false;
+        double yr = 0.0;
+        if (k < c1) {
+          const uint64_t b = bits(hsc, ctr0 + (uint64_t)k) >> 11;
+          if (phase == d) {
+            out[k] = (double)b * INV_2_53;                                 // prng.py:97-100
+          } else if (ndtri_classify(((double)b + 0.5) * INV_2_53, &yr, &neg)) {
+            out[k] = ndtri_central(yr);                                    // prng.py:103-111
+          } else {
+            tail = true;
+          }
+        }
+        phase += step;
+        if (phase >= per) phase -= per;
+        const unsigned bt = __ballot_sync(0xffffffffu, tail);
+        if (tail) {
+          const int pos = nt + __popc(bt & lt);
+          qy[pos] = yr;
+          qk[pos] = (unsigned)k | (neg ? 0x80000000u : 0u);
+        }
+        nt += __popc(bt);
+      }
+      __syncwarp();
+      for (int t = lane; t < nt; t += 32) {
+        const unsigned kk = qk[t];
+        out[kk & 0x7fffffffu] = ndtri_tail(qy[t], (kk >> 31) != 0);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+static cudaError_t launch_drmh_draws(const Params& p, int num_sms, cudaStream_t s) {
+  const int threads = 256, nw = threads / 32;
+  long long need = (p.st.m + nw - 1) / nw;
+  int blocks = (int)std::min<long long>(need, (long long)num_sms * 8);
+  drmh_draws_kernel<<<blocks, threads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t dispatch_drmh(int op, int g, int e, Params& p, const LaunchCtx& lc, cudaStream_t s,
                            uint64_t ps, long long off, const double* x0, double jit) {
   const int kind = p.t.kind;
+  if (op == 6) return launch_drmh_draws(p, lc.num_sms, s);
+  if (op == 5) {  // windowed run: the DR = true families
+    if (p.k.split_body) {
+#define X(GG, EE) \
+  if (g == GG && e == EE) return Launch<DrmhSplitW, GG, EE, 0>::window(p, lc, s);
+      FSMC_DRMH_SPLIT_CONFIGS(X)
+#undef X
+      return cudaErrorInvalidConfiguration;
+    }
+#define S(GG, EE, TK) \
+  if (g == GG && e == EE && kind == TK) return Launch<DrmhW, GG, EE, TK>::window(p, lc, s);
+    FSMC_DRMH_SPECIAL(S)
+#undef S
+#define X(GG, EE) \
+  if (g == GG && e == EE) return Launch<DrmhW, GG, EE, 0>::window(p, lc, s);
+    FSMC_DRMH_CONFIGS(X)
+#undef X
+    return cudaErrorInvalidConfiguration;
+  }
   if (p.k.split_body) {
 #define X(GG, EE) \
   if (g == GG && e == EE) return launch_op<DrmhSplit, GG, EE>(op, p, lc, s, ps, off, x0, jit);

@@ -390,7 +390,11 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
   p.variant = variant;
   p.mode = mode;
   int K = n_states(k);
-  for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
+  p.default_order = 1;
+  for (int i = 0; i < K; i++) {
+    p.order[i] = order ? order[i] : (i == 0 ? K : i);
+    if (p.order[i] != (i == 0 ? K : i)) p.default_order = 0;
+  }
   cudaStream_t cs = (cudaStream_t)stream_;
   p.next_chain = scratch().words;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
@@ -420,7 +424,11 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
   p.variant = variant;
   p.mode = mode;
   int K = n_states(k);
-  for (int i = 0; i < K; i++) p.order[i] = order ? order[i] : (i == 0 ? K : i);
+  p.default_order = 1;
+  for (int i = 0; i < K; i++) {
+    p.order[i] = order ? order[i] : (i == 0 ? K : i);
+    if (p.order[i] != (i == 0 ? K : i)) p.default_order = 0;
+  }
   p.b_lp = lp;
   p.b_grad = grad;
   p.b_theta = theta;
@@ -431,6 +439,57 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
   CUDA_TRY(cudaMemsetAsync(req_count, 0, sizeof(int32_t), cs));
   CUDA_TRY(dispatch_family(3, ge, p, cs));
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_run_windowed(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                              int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                              const fsmc_outputs* out, int64_t window, double* draws, int32_t lanes,
+                              void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (k->family != FSMC_DRMH) return fail(FSMC_ERR_UNSUPPORTED, "pre-drawn windows are for the DRMH kernels");
+  if (!draws || window < t->dim + 1 || window > 4096)
+    return fail(FSMC_ERR_ARG, "windowed run needs draws [m][window], dim + 1 <= window <= 4096");
+  if (n < 0) return fail(FSMC_ERR_ARG, "n must be >= 0");
+  if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
+  GE ge;
+  if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
+    return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = 1;
+  if (out) p.out = *out;
+  p.n = n;
+  p.tick_limit = tick_limit;
+  p.variant = variant;
+  p.mode = mode;
+  int K = n_states(k);
+  p.default_order = 1;
+  for (int i = 0; i < K; i++) {
+    p.order[i] = order ? order[i] : (i == 0 ? K : i);
+    if (p.order[i] != (i == 0 ? K : i)) p.default_order = 0;
+  }
+  p.draws = draws;
+  p.window = window;
+  cudaStream_t cs = (cudaStream_t)stream_;
+  unsigned* w = scratch().words;
+  p.next_chain = w;
+  p.unfinished = w + 8;
+  const int kCheck = 4;   // rounds between reads of the unfinished count
+  for (long long r = 0;; r++) {
+    CUDA_TRY(dispatch_family(6, ge, p, cs));
+    CUDA_TRY(cudaMemsetAsync(w, 0, sizeof(unsigned), cs));
+    CUDA_TRY(cudaMemsetAsync(p.unfinished, 0, sizeof(unsigned), cs));
+    CUDA_TRY(dispatch_family(5, ge, p, cs));
+    if (r % kCheck == kCheck - 1) {
+      unsigned left = 0;
+      CUDA_TRY(cudaMemcpyAsync(&left, p.unfinished, sizeof(unsigned), cudaMemcpyDeviceToHost, cs));
+      CUDA_TRY(cudaStreamSynchronize(cs));
+      if (!left) break;
+    }
+  }
   return FSMC_OK;
 }
 

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
     if (grp.lane == 0) {
       core_store(c, p, j);
       p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_STREAM] = (int64_t)stream;
+      p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_DRAW0] = (int64_t)c.ctr;
       if (!ok) report_error(c, p, j);
     }
   }
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
 // Every lane group pulls chains from a queue and runs each to completion
 // with its state in registers.  No barrier anywhere: chains in different
 // states simply execute different blocks.
-template <template <int, int> class F, int G, int E, int TK>
+template <template <int, int> class F, int G, int E, int TK, int VAR = 0>
 __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
@@ -134,11 +135,52 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Para
     const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
 #pragma unroll 1
     while (c.count < n_stop && c.tick < p.tick_limit)
-      if (!tick<F<G, E>, G, E, TK>(p, c, f, sm, j, grp)) { ok = false; break; }
+      if (!tick<F<G, E>, G, E, TK, false, VAR>(p, c, f, sm, j, grp)) { ok = false; break; }
     f.store(p, j, grp);
     if (grp.lane == 0) {
       core_store(c, p, j);
       if (!ok) report_error(c, p, j);
+    }
+  }
+}
+
+// ------------------------------------------------------------ windowed
+// fsm_run_kernel over pre-drawn windows (fsmc_run_windowed): the chain's
+// draws at counters dbase .. dbase + window - 1 are in p.draws[j]; it ticks
+// while a tick's worst case (dim + 1 draws for DRMH) still fits.
+template <template <int, int> class F, int G, int E, int TK, int VAR = 0>
+__global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_window_kernel(Params p) {
+  extern __shared__ double smem[];
+  Grp<G> grp;
+  // no cooperative-normal scratch: the draws are pre-generated, and the
+  // shared memory left unallocated becomes L1 for the draw windows
+  double* sm = smem + (threadIdx.x / G) * group_doubles(p.t);
+  double* ws = nullptr;
+  const long long lim = p.window - (p.t.dim + 1);
+  while (true) {
+    long long j = 0;
+    if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
+    j = grp.bcast_ll(j, 0);
+    if (j >= p.st.m) break;
+    Core c;
+    core_load(c, p, j);
+    c.ws = ws;
+    if (c.err_kind != FSMC_E_NONE) continue;
+    const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
+    if (c.count >= n_stop || c.tick >= p.tick_limit) continue;
+    c.dw = p.draws + (size_t)j * p.window;
+    c.dbase = c.ctr;
+    F<G, E> f;
+    f.load(p, j, grp);
+    bool ok = true;
+#pragma unroll 1
+    while (c.count < n_stop && c.tick < p.tick_limit && (long long)(c.ctr - c.dbase) <= lim)
+      if (!tick<F<G, E>, G, E, TK, false, VAR>(p, c, f, sm, j, grp)) { ok = false; break; }
+    f.store(p, j, grp);
+    if (grp.lane == 0) {
+      core_store(c, p, j);
+      if (!ok) report_error(c, p, j);
+      else if (c.count < n_stop && c.tick < p.tick_limit) atomicAdd(p.unfinished, 1u);
     }
   }
 }
@@ -330,30 +372,38 @@ struct Launch {
     fsm_init_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p, ps, off, x0, jit);
     return cudaGetLastError();
   }
-  static cudaError_t run(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
+  // a persistent chain-queue kernel with as many blocks as are co-resident
+  template <class KF>
+  static cudaError_t persistent(KF* kern, const Params& p, const LaunchCtx& lc, cudaStream_t s,
+                                size_t sm_bytes = 0) {
+    const size_t sb = sm_bytes ? sm_bytes : smem(p);
     int occ = 0;
-    cudaError_t e = allow_smem(fsm_run_kernel<F, G, E, TK>, smem(p));
+    cudaError_t e = allow_smem(kern, sb);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_run_kernel<F, G, E, TK>,
-                                                                  kThreads, smem(p));
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, sb);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
     int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
-    fsm_run_kernel<F, G, E, TK><<<blocks, kThreads, smem(p), s>>>(p);
+    kern<<<blocks, kThreads, sb, s>>>(p);
     return cudaGetLastError();
   }
+  static bool unrolled(const Params& p) {
+    return TK != 0 && p.variant == FSMC_BUNDLED && p.default_order;
+  }
+  static cudaError_t run(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
+    if constexpr (TK != 0)
+      if (unrolled(p)) return persistent(fsm_run_kernel<F, G, E, TK, 1>, p, lc, s);
+    return persistent(fsm_run_kernel<F, G, E, TK, 0>, p, lc, s);
+  }
   static cudaError_t profile(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
-    int occ = 0;
-    cudaError_t e = allow_smem(fsm_profile_kernel<F, G, E>, smem(p));
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_profile_kernel<F, G, E>, kThreads, smem(p));
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-    long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
-    int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
-    fsm_profile_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p);
-    return cudaGetLastError();
+    return persistent(fsm_profile_kernel<F, G, E>, p, lc, s);
+  }
+  static cudaError_t window(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
+    const size_t sb = std::max<size_t>(8, (size_t)(kThreads / G) * group_doubles(p.t) * sizeof(double));
+    if constexpr (TK != 0)
+      if (unrolled(p)) return persistent(fsm_window_kernel<F, G, E, TK, 1>, p, lc, s, sb);
+    return persistent(fsm_window_kernel<F, G, E, TK, 0>, p, lc, s, sb);
   }
   static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
@@ -391,7 +441,7 @@ struct Launch {
   }
 };
 
-// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile.  TK: compile-time plugin (0 = run-time switch)
+// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile (5 windowed run and 6 draws: fam_drmh.cu).  TK: compile-time plugin (0 = run-time switch)
 template <template <int, int> class F, int G, int E, int TK = 0>
 cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, uint64_t ps,
                       long long off, const double* x0, double jit) {

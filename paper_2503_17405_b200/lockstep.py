@@ -340,7 +340,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     cost_params: CostParams | None = None, tick_budget: int | None = None,
                     bundled_order: tuple | None = None, record_sample_ticks: bool = False,
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
-                    lanes: int = 0, evaluator=None, _timing: dict | None = None):
+                    lanes: int = 0, evaluator=None, draw_window: int = 0,
+                    _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
@@ -355,6 +356,10 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     ``evaluator="device"`` uses the per-point device plugin (bit-identical
     to the default mode).  Targets whose ``batched_evaluator()`` is not None
     (large dense designs) use it automatically.
+
+    ``draw_window`` (DRMH kernels): generate each chain's next ``draw_window``
+    PRNG draws in a separate full-occupancy kernel and let the step kernel
+    read them (``fsmc_run_windowed``); bit-identical to the inline draws.
     """
     _validate_run_args(batch, n)
     bundle.check_target(target)
@@ -381,7 +386,20 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
 
     if evaluator is None and hasattr(target, "batched_evaluator"):
         evaluator = target.batched_evaluator()
-    if evaluator is None:
+    if draw_window and (bundle.family != _lib.DRMH or evaluator is not None):
+        raise ValueError("draw_window applies to the DRMH kernels without an evaluator")
+    if draw_window:
+        # [m][window] plus a line of slack: the step kernel prefetches the
+        # next proposal's draws, which for the last chain may lie past its window
+        draws = torch.empty(m * int(draw_window) + 32, dtype=torch.float64, device="cuda")
+
+        def launch(mode, tick_limit):
+            _lib.check(lib.fsmc_run_windowed(ctypes.byref(kern), ctypes.byref(tgt),
+                                             ctypes.byref(batch.struct()), n, variant, ordv,
+                                             tick_limit, mode, ctypes.byref(out), int(draw_window),
+                                             draws.data_ptr(), lanes, _lib.stream_ptr()),
+                       "fsmc_run_windowed")
+    elif evaluator is None:
         def launch(mode, tick_limit):
             _lib.check(lib.fsmc_run(ctypes.byref(kern), ctypes.byref(tgt),
                                     ctypes.byref(batch.struct()), n, variant, ordv, tick_limit, mode,
