@@ -36,6 +36,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec & ESS/sec at m chains (1/2/4/8 B200); speed-up vs lock-step vmap"
+# executed fp64 flops per DRMH proposal on the MoG d=10 target (ncu SASS op
+# counts, DFMA counted twice: generator 65.1 per draw x 11 + step kernel 260)
+FP64_FLOPS_PER_PROPOSAL = 976.0
 
 CONFIGS = {
     "c2": dict(workload="C2: DRMH FSM, correlated MoG d=10 (rho=0.9, modes -3/0/3), M=100, "
@@ -322,21 +325,37 @@ def main():
            "d2h_bytes_per_step": 8 * (d + 2), "includes": "init_batch + run_fsm_batched + "
            "effective_sample_size (device) with host start point and host ESS summary"}
 
-    # roofline of the dominant kernel (fsm_run_kernel): algorithmic HBM bytes
+    # roofline of the run (fsm_run_kernel, or drmh_draws_kernel + fsm_window_kernel
+    # when the draws are generated ahead): algorithmic HBM bytes per launch
     kms = statistics.mean(kern_ms)
     evals = ledger.extras.get("evaluations", 0)
+    proposals = int(ledger.iter_counts.sum().item()) if hasattr(ledger.iter_counts, "sum") else 0
+    win = cfg.get("draw_window", 0) if cfg["family"] == "drmh" else 0
     st_bytes = 2 * m * 8 * (ledger_state_words(bundle, d))
     out_bytes = n * m * d * 8 + n * m * 4 * len(bundle.loop_states)
-    traffic_bytes = st_bytes + out_bytes
+    draw_bytes = 2 * 8 * (d + 1) * proposals if win else 0     # written once, read once
+    traffic_bytes = st_bytes + out_bytes + draw_bytes
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    pipe = json.load(open(os.path.join(ROOT, "profiles", "r01_pipe_peaks.json")))
     achieved = traffic_bytes / (kms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-            "kernel": "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel",
+            "kernel": ("drmh_draws_kernel + fsm_window_kernel<DrmhW,1,10,MOG>" if win else
+                       "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel"),
             "kernel_ms": kms, "algorithmic_bytes": traffic_bytes,
-            "note": "state in registers for the whole run: HBM carries only samples and "
-                    "ledger rows; the kernel is fp64/int issue-bound (see profiles/)"}
+            "note": "HBM carries samples, ledger rows, chain state and (windowed) the pre-drawn "
+                    "normals/uniforms, 16 B per draw; the run is fp64/integer issue-bound: see "
+                    "'compute' and profiles/"}
+    if cfg["family"] == "drmh" and proposals:
+        # executed fp64 flops per DRMH proposal (DFMA = 2), from ncu SASS counts of
+        # this pair of kernels (profiles/r01b_c2_ncu.md); peak = measured DFMA rate
+        fl = FP64_FLOPS_PER_PROPOSAL * proposals
+        ach_tf = fl / (kms / 1e3) / 1e12
+        roof["compute"] = {"pipe": "fp64", "achieved": ach_tf, "peak": pipe["fp64_fma_tflops"],
+                           "unit": "TFLOP/s", "frac": ach_tf / pipe["fp64_fma_tflops"],
+                           "flops_per_proposal": FP64_FLOPS_PER_PROPOSAL, "proposals": proposals,
+                           "peak_source": "profiles/r01_pipe_peaks.json (tools/peak_probe.cu)"}
 
     if cfg.get("batched"):
         # dominant work: the two contractions per evaluation, 4 N d flops each
