@@ -49,7 +49,8 @@ CONFIGS = {
     "c3": dict(workload="C3: NUTS FSM, equicorrelated Gaussian d=100 rho=0.99, eps=0.05, depth 10",
                family="nuts", m=16384, n=1000, d=100, variant="bundled", m_cpu=16),
     "c4": dict(workload="C4: elliptical slice FSM, GP-classification latent d=1024 (f-space)",
-               family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4),
+               family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4,
+               prior_transform="trmm"),
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; batched TF32 gradient evaluation across chains",
                family="nuts", m=131072, n=8, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
@@ -188,6 +189,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--draw-window", type=int, default=-1,
                     help="DRMH pre-drawn window in draws (0: inline generator; -1: config default)")
+    ap.add_argument("--prior", default="", choices=["", "none", "trmm", "gemm", "device"],
+                    help="ESS dense prior: batched nu = L eps per round (default: config's)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.m:
@@ -196,6 +199,8 @@ def main():
         cfg["n"] = args.n
     if args.draw_window >= 0:
         cfg["draw_window"] = args.draw_window
+    if args.prior:
+        cfg["prior_transform"] = None if args.prior == "none" else args.prior
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -241,7 +246,7 @@ def main():
         return fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
                                   output="torch", surplus=False, lanes=args.lanes,
                                   evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
-                                  _timing=timing)
+                                  prior_transform=cfg.get("prior_transform"), _timing=timing)
 
     held = None
     for s in range(args.warmup):
@@ -313,7 +318,8 @@ def main():
         batch = fm.init_batch(bundle, target, m, 500 + s, x0=x0, chain_offset=off)
         smp, _ = fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
                                     output="torch", surplus=False, lanes=args.lanes,
-                                    evaluator=evaluator, draw_window=cfg.get("draw_window", 0))
+                                    evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
+                                    prior_transform=cfg.get("prior_transform"))
         if has_ess:
             _ = fm.effective_sample_size(smp, burn=burn).pooled
         else:

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define FSMC_ABI_VERSION 2
+#define FSMC_ABI_VERSION 3
 #define FSMC_NINT 32        /* int64 slots per chain in fsmc_state.ints */
 #define FSMC_MAX_MODES 8    /* mixture components in FSMC_T_MOG */
 
@@ -218,6 +218,26 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
                          const fsmc_outputs* out, const double* lp, const double* grad,
                          double* theta, int32_t* req_chain, int32_t* req_count, int32_t lanes,
                          void* stream_);
+
+/* Batched prior transform (elliptical kernel, dense Gaussian prior): the
+ * INIT block's nu = L eps (elliptical.py:73, prng.py:114-136 normal_vec with
+ * chol) made one GEMM across chains.  Log densities are evaluated in place by
+ * the plugin (as fsmc_run); every chain runs until its next INIT, draws eps,
+ * and parks: req_chain[k] = j, nu[k][:] = eps, k = atomicAdd(req_count, 1).
+ * The caller overwrites each row with L eps (e.g. nu[:k] = nu[:k] @ L^T in
+ * one DGEMM, or fsmc_prior_apply below) and calls again; each chain resumes
+ * INIT from its transformed row.  Repeat until *req_count == 0.  Samples,
+ * ticks and ledger rows are those of fsmc_run (bit-identical with
+ * fsmc_prior_apply; within the GEMM's rounding otherwise). */
+fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                               int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                               const fsmc_outputs* out, double* nu, int32_t* req_chain,
+                               int32_t* req_count, int32_t lanes, void* stream_);
+
+/* nu[r][:] = L nu[r][:] in place for r < k (L = the target's dense prior
+ * factor), each row summed in the sampling kernel's order: the bit-exact
+ * prior transform for fsmc_advance_prior. */
+fsmc_status fsmc_prior_apply(const fsmc_target* t, double* nu, int64_t k, void* stream_);
 
 /* Logistic-regression evaluation epilogue over a tile of chains: given
  * Z [rows][N] = Theta X^T (fp32, from the contraction), labels y [N]:

@@ -15,7 +15,7 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FSMC_LIB", os.path.join(HERE, "libfsmc.so"))
 
-ABI_VERSION = 2    # fsmc.h FSMC_ABI_VERSION
+ABI_VERSION = 3    # fsmc.h FSMC_ABI_VERSION
 FSMC_NINT = 32
 MAX_MODES = 8
 
@@ -107,6 +107,13 @@ def lib():
                                ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Outputs),
                                _P, _P, _P, _P, _P, ctypes.c_int32, _P]
+    L.fsmc_advance_prior.restype = S
+    L.fsmc_advance_prior.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
+                                     ctypes.POINTER(State), ctypes.c_int64, ctypes.c_int32,
+                                     ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, ctypes.c_int32,
+                                     ctypes.POINTER(Outputs), _P, _P, _P, ctypes.c_int32, _P]
+    L.fsmc_prior_apply.restype = S
+    L.fsmc_prior_apply.argtypes = [ctypes.POINTER(Target), _P, ctypes.c_int64, _P]
     L.fsmc_lockstep_run.restype = S
     L.fsmc_lockstep_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                     ctypes.POINTER(State), ctypes.c_int64,

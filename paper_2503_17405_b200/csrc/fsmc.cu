@@ -402,14 +402,11 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
   return FSMC_OK;
 }
 
-fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
-                         int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
-                         const fsmc_outputs* out, const double* lp, const double* grad, double* theta,
-                         int32_t* req_chain, int32_t* req_count, int32_t lanes, void* stream_) {
-  fsmc_status s = check_args(k, t, st);
-  if (s != FSMC_OK) return s;
-  if (!theta || !req_chain || !req_count || !lp || (k->family == FSMC_NUTS && !grad))
-    return fail(FSMC_ERR_ARG, "advance needs theta, req_chain, req_count, lp (and grad for NUTS)");
+static fsmc_status advance_common(int op, const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                                  int64_t n, int32_t variant, const int32_t* order, int64_t tick_limit,
+                                  int32_t mode, const fsmc_outputs* out, const double* lp,
+                                  const double* grad, double* theta, int32_t* req_chain,
+                                  int32_t* req_count, int32_t lanes, void* stream_) {
   if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
   GE ge;
   if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
@@ -434,11 +431,66 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
   p.b_theta = theta;
   p.b_req_chain = req_chain;
   p.b_req_count = req_count;
+  p.b_prior = op == 7;
   cudaStream_t cs = (cudaStream_t)stream_;
   p.next_chain = scratch().words;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
   CUDA_TRY(cudaMemsetAsync(req_count, 0, sizeof(int32_t), cs));
-  CUDA_TRY(dispatch_family(3, ge, p, cs));
+  CUDA_TRY(dispatch_family(op, ge, p, cs));
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                         int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                         const fsmc_outputs* out, const double* lp, const double* grad, double* theta,
+                         int32_t* req_chain, int32_t* req_count, int32_t lanes, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (!theta || !req_chain || !req_count || !lp || (k->family == FSMC_NUTS && !grad))
+    return fail(FSMC_ERR_ARG, "advance needs theta, req_chain, req_count, lp (and grad for NUTS)");
+  return advance_common(3, k, t, st, n, variant, order, tick_limit, mode, out, lp, grad, theta,
+                        req_chain, req_count, lanes, stream_);
+}
+
+fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                               int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                               const fsmc_outputs* out, double* nu, int32_t* req_chain,
+                               int32_t* req_count, int32_t lanes, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (k->family != FSMC_ESS || t->prior_kind != FSMC_PRIOR_DENSE)
+    return fail(FSMC_ERR_UNSUPPORTED, "the batched prior transform is for the elliptical kernel with a dense prior");
+  if (!nu || !req_chain || !req_count)
+    return fail(FSMC_ERR_ARG, "advance_prior needs nu, req_chain, req_count");
+  return advance_common(7, k, t, st, n, variant, order, tick_limit, mode, out, nullptr, nullptr, nu,
+                        req_chain, req_count, lanes, stream_);
+}
+
+// nu[r] = L nu[r] in place, every row summed in the sampling kernel's order
+// (k ascending, one fma per term): the bit-exact batched prior transform
+__global__ void __launch_bounds__(256) prior_apply_kernel(const double* __restrict__ Lt, double* nu, int d) {
+  extern __shared__ double eps[];
+  double* row = nu + (size_t)blockIdx.x * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) eps[i] = row[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k <= i; k++) acc = fma(__ldg(&Lt[(size_t)k * d + i]), eps[k], acc);
+    row[i] = acc;
+  }
+}
+
+fsmc_status fsmc_prior_apply(const fsmc_target* t, double* nu, int64_t k, void* stream_) {
+  if (!t || !nu || k < 0) return fail(FSMC_ERR_ARG, "prior_apply needs a target and nu");
+  if (t->prior_kind != FSMC_PRIOR_DENSE || !t->prior_t)
+    return fail(FSMC_ERR_ARG, "prior_apply needs a dense prior factor");
+  if (k == 0) return FSMC_OK;
+  const size_t sb = (size_t)t->dim * sizeof(double);
+  if (sb > 48 * 1024)
+    CUDA_TRY(cudaFuncSetAttribute((const void*)prior_apply_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  prior_apply_kernel<<<(unsigned)k, 256, sb, (cudaStream_t)stream_>>>(t->prior_t, nu, (int)t->dim);
+  CUDA_TRY(cudaGetLastError());
   return FSMC_OK;
 }
 

@@ -48,7 +48,7 @@ inline cudaError_t allow_smem(K* kern, size_t bytes) {
 #define FSMC_WARP_MIN_BLOCKS 3
 #endif
 template <int G>
-__host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : (G == 32 ? FSMC_WARP_MIN_BLOCKS : 1); }
+__host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : (G == 32 ? FSMC_WARP_MIN_BLOCKS : (G == 128 ? 4 : 1)); }
 
 struct LaunchCtx {
   int num_sms;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_profile_kernel(
 // ------------------------------------------------------------- advance
 // Batched-evaluation mode: every chain runs to its next log-density request
 // and parks the point in the compact request list (see fsmc_advance).
-template <template <int, int> class F, int G, int E>
+template <template <int, int> class F, int G, int E, int TK = 0, bool INLINE = false>
 __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_advance_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_advance_kernel(
     f.load(p, j, grp);
     long long resume = p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_RESUME];
     bool ok = true;
-    advance_chain<F<G, E>, G, E>(p, c, f, sm, j, grp, resume, ok);
+    advance_chain<F<G, E>, G, E, TK, INLINE>(p, c, f, sm, j, grp, resume, ok);
     f.store(p, j, grp);
     if (grp.lane == 0) {
       core_store(c, p, j);
@@ -406,17 +406,11 @@ struct Launch {
     return persistent(fsm_window_kernel<F, G, E, TK, 0>, p, lc, s, sb);
   }
   static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
-    int occ = 0;
-    cudaError_t e = allow_smem(fsm_advance_kernel<F, G, E>, smem(p));
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsm_advance_kernel<F, G, E>,
-                                                                  kThreads, smem(p));
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-    long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
-    int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
-    fsm_advance_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p);
-    return cudaGetLastError();
+    return persistent(fsm_advance_kernel<F, G, E>, p, lc, s);
+  }
+  // fsmc_advance_prior: evaluations inline, parked only at the prior transform
+  static cudaError_t advance_prior(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
+    return persistent(fsm_advance_kernel<F, G, E, TK, true>, p, lc, s);
   }
   static cudaError_t lockstep(Params p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
@@ -441,7 +435,7 @@ struct Launch {
   }
 };
 
-// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile (5 windowed run and 6 draws: fam_drmh.cu).  TK: compile-time plugin (0 = run-time switch)
+// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile, 7 advance with batched prior (5 windowed run and 6 draws: fam_drmh.cu).  TK: compile-time plugin (0 = run-time switch)
 template <template <int, int> class F, int G, int E, int TK = 0>
 cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, uint64_t ps,
                       long long off, const double* x0, double jit) {
@@ -449,6 +443,10 @@ cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, ui
   if (op == 1) return Launch<F, G, E, TK>::run(p, lc, s);
   if (op == 3) return Launch<F, G, E, 0>::advance(p, lc, s);
   if (op == 4) return Launch<F, G, E, 0>::profile(p, lc, s);
+  if (op == 7) {
+    if constexpr (F<G, E>::PRIOR) return Launch<F, G, E, TK>::advance_prior(p, lc, s);
+    return cudaErrorInvalidConfiguration;
+  }
   return Launch<F, G, E, TK>::lockstep(p, lc, s);
 }
 

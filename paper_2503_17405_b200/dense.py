@@ -101,3 +101,62 @@ class LogisticRegressionEvaluator:
         if st != 0:
             raise RuntimeError("fsmc_logreg_tc_eval: " +
                                _lib.lib().fsmc_logreg_tc_last_error().decode())
+
+
+# ---------------------------------------------------------------- prior transform
+# Elliptical slice sampling with a dense Gaussian prior draws nu = L eps at
+# every INIT (elliptical.py:73).  In fsmc_advance_prior mode the parked eps
+# rows of a round are transformed together: one triangular matrix product
+# across chains (cuBLAS DTRMM, d^2 flops per row instead of a GEMV per chain).
+_CUBLAS = None
+
+
+def _cublas():
+    global _CUBLAS
+    if _CUBLAS is None:
+        import ctypes
+        import os
+
+        import nvidia.cublas as nc
+        lib = ctypes.CDLL(os.path.join(list(nc.__path__)[0], "lib", "libcublas.so.12"))
+        P = ctypes.c_void_p
+        lib.cublasDtrmm_v2.restype = ctypes.c_int
+        lib.cublasDtrmm_v2.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                       P, ctypes.c_int, P, ctypes.c_int, P, ctypes.c_int]
+        _CUBLAS = lib
+    return _CUBLAS
+
+
+class PriorTransform:
+    """nu[r] = L nu[r] for the rows of a round, L lower-triangular (the
+    target's prior factor; ``Lt`` = Lᵀ row-major = L column-major).
+    ``method="trmm"``: cuBLAS DTRMM (half the flops of a dense product);
+    ``"gemm"``: a dense DGEMM ``rows @ Lᵀ``."""
+
+    def __init__(self, Lt: torch.Tensor, method: str = "trmm"):
+        if method not in ("trmm", "gemm"):
+            raise ValueError("method must be trmm or gemm")
+        self.Lt, self.method, self.d = Lt, method, Lt.shape[0]
+        self.tmp = None
+        self.one = None
+
+    def __call__(self, rows: torch.Tensor) -> None:
+        k, d = rows.shape
+        if self.tmp is None or self.tmp.shape[0] < k:
+            self.tmp = torch.empty_like(rows)
+        out = self.tmp[:k]
+        if self.method == "gemm":
+            torch.mm(rows, self.Lt, out=out)
+        else:
+            import ctypes
+            if self.one is None:
+                self.one = ctypes.c_double(1.0)
+            h = torch.cuda.current_blas_handle()     # bound to the current stream
+            # column-major: C (d x k) = L (d x d, lower) * B (d x k); B = rows
+            st = _cublas().cublasDtrmm_v2(h, 0, 0, 0, 0, d, k, ctypes.byref(self.one),
+                                          self.Lt.data_ptr(), d, rows.data_ptr(), d,
+                                          out.data_ptr(), d)
+            if st != 0:
+                raise RuntimeError(f"cublasDtrmm failed ({st})")
+        rows.copy_(out)

@@ -341,7 +341,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     bundled_order: tuple | None = None, record_sample_ticks: bool = False,
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
                     lanes: int = 0, evaluator=None, draw_window: int = 0,
-                    _timing: dict | None = None):
+                    prior_transform=None, _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
@@ -356,6 +356,16 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     ``evaluator="device"`` uses the per-point device plugin (bit-identical
     to the default mode).  Targets whose ``batched_evaluator()`` is not None
     (large dense designs) use it automatically.
+
+    ``prior_transform`` (elliptical kernel with a dense Gaussian prior):
+    batch the INIT block's nu = L eps across chains (``fsmc_advance_prior``).
+    Chains run with the plugin evaluated in place until their next INIT,
+    park eps, and all parked rows are transformed in one call.  "gemm": one
+    fp64 GEMM ``eps @ L^T`` (cuBLAS DGEMM; values within its rounding);
+    "trmm": the same product as a triangular cuBLAS DTRMM (half the flops);
+    "device": ``fsmc_prior_apply``, the sampling kernel's summation order
+    (bit-identical to the default mode); or a callable ``f(nu[k, d])``
+    transforming the rows in place.
 
     ``draw_window`` (DRMH kernels): generate each chain's next ``draw_window``
     PRNG draws in a separate full-occupancy kernel and let the step kernel
@@ -388,7 +398,16 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         evaluator = target.batched_evaluator()
     if draw_window and (bundle.family != _lib.DRMH or evaluator is not None):
         raise ValueError("draw_window applies to the DRMH kernels without an evaluator")
-    if draw_window:
+    if prior_transform is not None:
+        gp = getattr(target, "gaussian_prior", None)
+        if bundle.family != _lib.ESS or gp is None or evaluator is not None or draw_window:
+            raise ValueError("prior_transform applies to the elliptical kernel with a Gaussian "
+                             "prior, without an evaluator")
+        if target.struct().prior_kind != _lib.PRIOR_DENSE:
+            prior_transform = None      # identity prior: nu = eps, nothing to batch
+    if prior_transform is not None:
+        launch = _prior_launcher(target, batch, n, variant, ordv, out, lanes, prior_transform)
+    elif draw_window:
         # [m][window] plus a line of slack: the step kernel prefetches the
         # next proposal's draws, which for the last chain may lie past its window
         draws = torch.empty(m * int(draw_window) + 32, dtype=torch.float64, device="cuda")
@@ -495,6 +514,44 @@ def _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evalu
             stats["rounds"] += 1
             stats["evaluations"] += k
             evaluator(theta[:k], lp[:k], None if g is None else g[:k])
+
+    launch.stats = stats
+    return launch
+
+
+def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform):
+    """Rounds of fsmc_advance_prior + one batched nu = L eps over every
+    chain parked at INIT."""
+    m, d = batch.m, target.dim
+    nu = torch.empty((m, d), dtype=torch.float64, device="cuda")
+    req_chain = torch.empty(m, dtype=torch.int32, device="cuda")
+    req_count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib = _lib.lib()
+    kern, tgt = batch.kernel, target.struct()
+    if transform in ("gemm", "trmm"):
+        from .dense import PriorTransform
+        transform = PriorTransform(target.device_arrays()["prior_t"], transform)
+    elif transform == "device":
+        def transform(rows):
+            _lib.check(lib.fsmc_prior_apply(ctypes.byref(tgt), rows.data_ptr(), rows.shape[0],
+                                            _lib.stream_ptr()), "fsmc_prior_apply")
+    elif not callable(transform):
+        raise ValueError("prior_transform must be 'trmm', 'gemm', 'device' or a callable")
+    stats = {"rounds": 0, "prior_transforms": 0}
+
+    def launch(mode, tick_limit):
+        while True:
+            _lib.check(lib.fsmc_advance_prior(ctypes.byref(kern), ctypes.byref(tgt),
+                                              ctypes.byref(batch.struct()), n, variant, ordv,
+                                              tick_limit, mode, ctypes.byref(out), nu.data_ptr(),
+                                              req_chain.data_ptr(), req_count.data_ptr(), lanes,
+                                              _lib.stream_ptr()), "fsmc_advance_prior")
+            k = int(req_count.item())
+            if k == 0:
+                return
+            stats["rounds"] += 1
+            stats["prior_transforms"] += k
+            transform(nu[:k])
 
     launch.stats = stats
     return launch
