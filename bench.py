@@ -54,7 +54,7 @@ CONFIGS = {
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; batched TF32 gradient evaluation across chains",
                family="nuts", m=131072, n=8, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
-               batched="bf16-tc"),
+               batched="bf16-tc", n_lock=2),
 }
 
 
@@ -290,23 +290,31 @@ def main():
         ess_per_sec = ess.pooled / (t_total / args.steps)
 
     # lock-step (vmap-style) baseline, same code, same chains
+    # (batched configs: the same evaluator in fsmc_advance_lockstep rounds, a
+    # barrier at every sample; n_lock samples per chain bound its run time)
     lock = None
-    if not args.no_lockstep and not cfg.get("batched"):
-        lock_ms = []
-        for s in range(2):
+    if not args.no_lockstep:
+        lock_ms, lock_extra = [], {}
+        n_lock = min(n, cfg.get("n_lock", n))
+        for s in range(1 if cfg.get("batched") else 2):
             flush.fill_(s)
             barrier()
             batch = fm.init_batch(bundle, target, m, s, chain_offset=off)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            fm.run_standard_batched(bundle, target, batch, n, output="torch", lanes=args.lanes)
+            _, lled = fm.run_standard_batched(bundle, target, batch, n_lock, output="torch",
+                                              lanes=args.lanes, evaluator=evaluator)
             e1.record()
             barrier()
             lock_ms.append(e0.elapsed_time(e1))
+            lock_extra = dict(lled.extras)
         t_lock = max_over_ranks(min(lock_ms) / 1e3)
-        lock_value = world * m * n / t_lock
+        lock_value = world * m * n_lock / t_lock
         lock = {"value": lock_value, "unit": "samples/s", "ms_per_step": 1e3 * t_lock,
-                "speedup": value / lock_value}
+                "speedup": value / lock_value, "n": n_lock, **lock_extra}
+        if cfg.get("prior_transform"):
+            lock["note"] = ("lock-step kernel forms nu = L eps per chain (no batched prior "
+                            "transform); FSM with the same per-chain transform: see --prior none")
 
     # end-to-end through the public API: host x0 (pinned) -> device, run, ESS -> host
     x0_host = torch.zeros(d, dtype=torch.float64).pin_memory()

@@ -219,6 +219,21 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
                          double* theta, int32_t* req_chain, int32_t* req_count, int32_t lanes,
                          void* stream_);
 
+/* Lock-step baseline in batched-evaluation mode (run_standard_batched with an
+ * evaluator; vmap semantics of the monolithic samplers, lockstep.py:238-305):
+ * as fsmc_advance (plain executor, mode 0), but no chain starts sample s + 1
+ * until every chain has finished sample s, and a chain waiting at that
+ * barrier appends an idle request (its current point; the result is
+ * discarded), as a vmapped while loop evaluates the whole batch each
+ * iteration.  level [2] int64: set level[1] = 0 before the first call; each
+ * call moves level[1] to level[0] and leaves the minimum sample count over
+ * the (non-failed) chains in level[1].  Repeat until *req_count == 0.
+ * Samples and per-sample counts equal the FSM run's. */
+fsmc_status fsmc_advance_lockstep(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                  const fsmc_outputs* out, const double* lp, const double* grad,
+                                  double* theta, int32_t* req_chain, int32_t* req_count, int64_t* level,
+                                  int32_t lanes, void* stream_);
+
 /* Batched prior transform (elliptical kernel, dense Gaussian prior): the
  * INIT block's nu = L eps (elliptical.py:73, prng.py:114-136 normal_vec with
  * chol) made one GEMM across chains.  Log densities are evaluated in place by

@@ -107,6 +107,11 @@ def lib():
                                ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Outputs),
                                _P, _P, _P, _P, _P, ctypes.c_int32, _P]
+    L.fsmc_advance_lockstep.restype = S
+    L.fsmc_advance_lockstep.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
+                                        ctypes.POINTER(State), ctypes.c_int64,
+                                        ctypes.POINTER(Outputs), _P, _P, _P, _P, _P, _P,
+                                        ctypes.c_int32, _P]
     L.fsmc_advance_prior.restype = S
     L.fsmc_advance_prior.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                      ctypes.POINTER(State), ctypes.c_int64, ctypes.c_int32,

@@ -32,21 +32,21 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
       const int c1 = min(W, c0 + kDrawChunk);
       int nt = 0;
       for (int k0 = c0; k0 < c1; k0 += 32) {
+        // branch-free: every lane evaluates the central branch (uniform and
+        // tail lanes discard it), so the warp never splits three ways
         const int k = k0 + lane;
-        bool tail = false, neg = false;
-        double yr = 0.0;
-        if (k < c1) {
-          const uint64_t b = bits(hsc, ctr0 + (uint64_t)k) >> 11;
-          if (phase == d) {
-            out[k] = (double)b * INV_2_53;                                 // prng.py:97-100
-          } else if (ndtri_classify(((double)b + 0.5) * INV_2_53, &yr, &neg)) {
-            out[k] = ndtri_central(yr);                                    // prng.py:103-111
-          } else {
-            tail = true;
-          }
-        }
+        const bool live = k < c1;
+        const double bd = (double)(bits(hsc, ctr0 + (uint64_t)k) >> 11);
+        const bool uni = phase == d;
+        bool neg;
+        double yr;
+        const bool central = ndtri_classify((bd + 0.5) * INV_2_53, &yr, &neg);  // prng.py:103-111
+        const double vc = ndtri_central(yr);
+        const double v = uni ? bd * INV_2_53 : vc;                               // prng.py:97-100
+        const bool tail = live && !uni && !central;
+        if (live && !tail) out[k] = v;
         phase += step;
-        if (phase >= per) phase -= per;
+        phase = phase >= per ? phase - per : phase;
         const unsigned bt = __ballot_sync(0xffffffffu, tail);
         if (tail) {
           const int pos = nt + __popc(bt & lt);

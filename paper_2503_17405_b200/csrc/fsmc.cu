@@ -406,7 +406,8 @@ static fsmc_status advance_common(int op, const fsmc_kernel* k, const fsmc_targe
                                   int64_t n, int32_t variant, const int32_t* order, int64_t tick_limit,
                                   int32_t mode, const fsmc_outputs* out, const double* lp,
                                   const double* grad, double* theta, int32_t* req_chain,
-                                  int32_t* req_count, int32_t lanes, void* stream_) {
+                                  int32_t* req_count, int32_t lanes, void* stream_,
+                                  int64_t* level = nullptr) {
   if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
   GE ge;
   if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
@@ -432,7 +433,12 @@ static fsmc_status advance_common(int op, const fsmc_kernel* k, const fsmc_targe
   p.b_req_chain = req_chain;
   p.b_req_count = req_count;
   p.b_prior = op == 7;
+  p.b_level = (long long*)level;
   cudaStream_t cs = (cudaStream_t)stream_;
+  if (level) {  // this round's barrier level = last round's minimum count
+    CUDA_TRY(cudaMemcpyAsync(level, level + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, cs));
+    CUDA_TRY(cudaMemsetAsync(level + 1, 0x7f, sizeof(int64_t), cs));
+  }
   p.next_chain = scratch().words;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
   CUDA_TRY(cudaMemsetAsync(req_count, 0, sizeof(int32_t), cs));
@@ -450,6 +456,18 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
     return fail(FSMC_ERR_ARG, "advance needs theta, req_chain, req_count, lp (and grad for NUTS)");
   return advance_common(3, k, t, st, n, variant, order, tick_limit, mode, out, lp, grad, theta,
                         req_chain, req_count, lanes, stream_);
+}
+
+fsmc_status fsmc_advance_lockstep(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                  const fsmc_outputs* out, const double* lp, const double* grad,
+                                  double* theta, int32_t* req_chain, int32_t* req_count, int64_t* level,
+                                  int32_t lanes, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (!theta || !req_chain || !req_count || !lp || !level || (k->family == FSMC_NUTS && !grad))
+    return fail(FSMC_ERR_ARG, "advance_lockstep needs theta, req_chain, req_count, lp, level (and grad for NUTS)");
+  return advance_common(3, k, t, st, n, FSMC_PLAIN, nullptr, INT64_MAX, 0, out, lp, grad, theta,
+                        req_chain, req_count, lanes, stream_, level);
 }
 
 fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,

@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_advance_kernel(
     f.store(p, j, grp);
     if (grp.lane == 0) {
       core_store(c, p, j);
+      if (p.b_level && ok) atomicMin((unsigned long long*)&p.b_level[1], (unsigned long long)c.count);
       p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_RESUME] = resume;
       if (!ok) report_error(c, p, j);
     }

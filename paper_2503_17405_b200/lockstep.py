@@ -578,9 +578,16 @@ def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks,
 
 def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
                          cost_params: CostParams | None = None, *, output: str = "numpy",
-                         lanes: int = 0):
+                         lanes: int = 0, evaluator=None):
     """Lock-step baseline: one monolithic sample per chain per iteration with
-    barrier semantics (lockstep.py:238-305), on the device."""
+    barrier semantics (lockstep.py:238-305), on the device.
+
+    ``evaluator``: the lock-step baseline of the batched-evaluation mode
+    (``fsmc_advance_lockstep``): every round evaluates one point per chain in
+    one call, and no chain starts its next sample until all chains finished
+    the current one (chains waiting at the barrier submit idle points, as a
+    vmapped while loop evaluates the whole batch).  Same evaluator contract
+    as ``run_fsm_batched``; "device" = the per-point plugin."""
     _validate_run_args(batch, n)
     bundle.check_target(target)
     params = cost_params or bundle.default_costs
@@ -596,12 +603,18 @@ def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
     m, d = batch.m, target.dim
     rec = bundle.loop_states
     samples, loops, _, out = _outputs(n, m, d, len(rec), False)
+    if evaluator is None and hasattr(target, "batched_evaluator"):
+        evaluator = target.batched_evaluator()
+    stats = None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    _lib.check(_lib.lib().fsmc_lockstep_run(ctypes.byref(batch.kernel),
-                                            ctypes.byref(target.struct()),
-                                            ctypes.byref(batch.struct()), n, ctypes.byref(out),
-                                            lanes, _lib.stream_ptr()), "fsmc_lockstep_run")
+    if evaluator is None:
+        _lib.check(_lib.lib().fsmc_lockstep_run(ctypes.byref(batch.kernel),
+                                                ctypes.byref(target.struct()),
+                                                ctypes.byref(batch.struct()), n, ctypes.byref(out),
+                                                lanes, _lib.stream_ptr()), "fsmc_lockstep_run")
+    else:
+        stats = _lockstep_batched(bundle, target, batch, n, out, lanes, evaluator)
     torch.cuda.synchronize()
     walltime = time.perf_counter() - t0
     batch.active_mask = [False] * m
@@ -625,7 +638,39 @@ def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
     ledger = CostLedger(iter_counts=_convert(it, output), loop_exec_counts=loop_execs,
                         tick_count=n, block_exec_counts=_convert(blocks, output),
                         charged_cost=charged, walltime=walltime, regime="standard")
+    if stats is not None:
+        ledger.extras.update(stats)
     return _convert(samples, output), ledger
+
+
+def _lockstep_batched(bundle, target, batch, n, out, lanes, evaluator) -> dict:
+    """Rounds of fsmc_advance_lockstep + one batched evaluation each."""
+    m, d = batch.m, target.dim
+    if evaluator == "device":
+        evaluator = _device_evaluator(target, bundle.family, lanes)
+    grad = bundle.family == _lib.NUTS
+    theta = torch.empty((m, d), dtype=torch.float64, device="cuda")
+    lp = torch.empty(m, dtype=torch.float64, device="cuda")
+    g = torch.empty((m, d), dtype=torch.float64, device="cuda") if grad else None
+    req_chain = torch.empty(m, dtype=torch.int32, device="cuda")
+    req_count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    level = torch.zeros(2, dtype=torch.int64, device="cuda")
+    lib = _lib.lib()
+    kern, tgt = batch.kernel, target.struct()
+    stats = {"rounds": 0, "evaluations": 0}
+    while True:
+        _lib.check(lib.fsmc_advance_lockstep(ctypes.byref(kern), ctypes.byref(tgt),
+                                             ctypes.byref(batch.struct()), n, ctypes.byref(out),
+                                             lp.data_ptr(), _lib.ptr(g), theta.data_ptr(),
+                                             req_chain.data_ptr(), req_count.data_ptr(),
+                                             level.data_ptr(), lanes, _lib.stream_ptr()),
+                   "fsmc_advance_lockstep")
+        k = int(req_count.item())
+        if k == 0:
+            return stats
+        stats["rounds"] += 1
+        stats["evaluations"] += k
+        evaluator(theta[:k], lp[:k], None if g is None else g[:k])
 
 
 def measure_block_costs(bundle, target, m: int = 8, seed: int = 0, ticks: int = 200) -> CostParams:
