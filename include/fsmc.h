@@ -219,15 +219,31 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
                          double* theta, int32_t* req_chain, int32_t* req_count, int32_t lanes,
                          void* stream_);
 
+/* Deferred init (targets evaluated only by a batched evaluator, e.g. the GP
+ * hyperparameter target above 56 observations): fsmc_init_deferred is
+ * fsmc_init (init_batch, lockstep.py:175-206: streams, jitter draws, x0)
+ * without the starting point's evaluation; the caller evaluates every
+ * chain's starting point x = vec[j][0][:] in one batched call and passes
+ * the log densities lp [m] to fsmc_init_finish, which runs the Locals
+ * constructor's checks (BlockFailure / TargetError records) as fsmc_init. */
+fsmc_status fsmc_init_deferred(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                               uint64_t parent_stream, int64_t chain_offset, const double* x0,
+                               double init_jitter, void* stream_);
+fsmc_status fsmc_init_finish(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, const double* lp,
+                             void* stream_);
+
 /* Lock-step baseline in batched-evaluation mode (run_standard_batched with an
  * evaluator; vmap semantics of the monolithic samplers, lockstep.py:238-305):
  * as fsmc_advance (plain executor, mode 0), but no chain starts sample s + 1
  * until every chain has finished sample s, and a chain waiting at that
  * barrier appends an idle request (its current point; the result is
  * discarded), as a vmapped while loop evaluates the whole batch each
- * iteration.  level [2] int64: set level[1] = 0 before the first call; each
- * call moves level[1] to level[0] and leaves the minimum sample count over
- * the (non-failed) chains in level[1].  Repeat until *req_count == 0.
+ * iteration.  level [3] int64: set level[1] = 0 before the first call; each
+ * call moves level[1] to level[0], leaves the minimum sample count over the
+ * (non-failed) chains in level[1] and the number of real (non-idle) requests
+ * in level[2].  A round whose requests are all idle (the slowest chains
+ * finished their sample without a new request) needs no evaluation: vmap
+ * would start the next iteration at once.  Repeat until *req_count == 0.
  * Samples and per-sample counts equal the FSM run's. */
 fsmc_status fsmc_advance_lockstep(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                                   const fsmc_outputs* out, const double* lp, const double* grad,

@@ -107,6 +107,11 @@ def lib():
                                ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Outputs),
                                _P, _P, _P, _P, _P, ctypes.c_int32, _P]
+    L.fsmc_init_deferred.restype = S
+    L.fsmc_init_deferred.argtypes = list(L.fsmc_init.argtypes)
+    L.fsmc_init_finish.restype = S
+    L.fsmc_init_finish.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
+                                   ctypes.POINTER(State), _P, _P]
     L.fsmc_advance_lockstep.restype = S
     L.fsmc_advance_lockstep.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                         ctypes.POINTER(State), ctypes.c_int64,

@@ -308,10 +308,14 @@ fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_st
     return fail(FSMC_ERR_ARG, "slice sampling here is univariate");
   if (k->family == FSMC_ESS && t->prior_kind == FSMC_PRIOR_NONE)
     return fail(FSMC_ERR_ARG, "elliptical slice sampling needs a Gaussian-prior split");
+  // scratch == 0: no per-chain plugin (more than kGpMaxRows observations), the
+  // evaluations come from a batched evaluator (the plugin reports a TargetError)
   if (t->kind == FSMC_T_GP_HYPER &&
-      (t->dim != 3 || t->n_rows < 2 || t->n_rows > kGpMaxRows || !t->data || !t->yvec ||
-       t->scratch < 2 * t->n_rows * t->n_rows + 2 * t->n_rows + 4))
-    return fail(FSMC_ERR_ARG, "GP target: dim 3, 2 <= n <= 56 observations, scratch 2n^2+2n+4");
+      (t->dim != 3 || t->n_rows < 2 || !t->data || !t->yvec ||
+       (t->scratch != 0 && (t->n_rows > kGpMaxRows ||
+                            t->scratch < 2 * t->n_rows * t->n_rows + 2 * t->n_rows + 4))))
+    return fail(FSMC_ERR_ARG, "GP target: dim 3, n >= 2 observations; the per-chain plugin needs "
+                              "n <= 56 and scratch 2n^2+2n+4 (scratch 0: batched evaluator only)");
   if (t->kind == FSMC_T_MOG && (t->n_modes < 1 || t->n_modes > FSMC_MAX_MODES))
     return fail(FSMC_ERR_ARG, "n_modes out of range");
   return FSMC_OK;
@@ -354,8 +358,9 @@ fsmc_status fsmc_prng_fill(uint64_t seed, uint64_t stream, uint64_t counter, int
   return FSMC_OK;
 }
 
-fsmc_status fsmc_init(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, uint64_t parent_stream,
-                      int64_t chain_offset, const double* x0, double init_jitter, void* stream_) {
+static fsmc_status init_common(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                               uint64_t parent_stream, int64_t chain_offset, const double* x0,
+                               double init_jitter, void* stream_, bool defer) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   GE ge;
@@ -364,9 +369,37 @@ fsmc_status fsmc_init(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st
   memset(&p, 0, sizeof(p));
   p.k = *k; p.t = *t; p.st = *st;
   p.t.full = k->family != FSMC_ESS;
+  p.b_defer = defer;
   cudaStream_t cs = (cudaStream_t)stream_;
   CUDA_TRY(cudaMemsetAsync(st->err_key, 0xff, sizeof(unsigned long long), cs));
   CUDA_TRY(dispatch_family(0, ge, p, cs, parent_stream, chain_offset, x0, init_jitter));
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_init(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, uint64_t parent_stream,
+                      int64_t chain_offset, const double* x0, double init_jitter, void* stream_) {
+  return init_common(k, t, st, parent_stream, chain_offset, x0, init_jitter, stream_, false);
+}
+
+fsmc_status fsmc_init_deferred(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                               uint64_t parent_stream, int64_t chain_offset, const double* x0,
+                               double init_jitter, void* stream_) {
+  return init_common(k, t, st, parent_stream, chain_offset, x0, init_jitter, stream_, true);
+}
+
+fsmc_status fsmc_init_finish(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, const double* lp,
+                             void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (!lp) return fail(FSMC_ERR_ARG, "init_finish needs lp [m]");
+  GE ge;
+  if (!pick_config(k->family, t->dim, 0, ge, t->kind)) return fail(FSMC_ERR_UNSUPPORTED, "dimension not supported");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = k->family != FSMC_ESS;
+  p.b_init_lp = lp;
+  CUDA_TRY(dispatch_family(8, ge, p, (cudaStream_t)stream_));
   return FSMC_OK;
 }
 
@@ -438,6 +471,7 @@ static fsmc_status advance_common(int op, const fsmc_kernel* k, const fsmc_targe
   if (level) {  // this round's barrier level = last round's minimum count
     CUDA_TRY(cudaMemcpyAsync(level, level + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, cs));
     CUDA_TRY(cudaMemsetAsync(level + 1, 0x7f, sizeof(int64_t), cs));
+    CUDA_TRY(cudaMemsetAsync(level + 2, 0, sizeof(int64_t), cs));
   }
   p.next_chain = scratch().words;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));

@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
     if constexpr (F<G, E>::SHAPE == SHAPE_NESTED) {
       f.init_state();
       f.ck = nullptr;
+    } else if (p.b_defer) {
+      f.init_pre();   // the evaluation point is x (vec row 0); fsm_init_finish_kernel completes
     } else {
       f.init_pre();
       double lp = target_eval<G, E, false>(p.t, f.ev(), f.evg(), sm, grp);
@@ -105,6 +107,38 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
       core_store(c, p, j);
       p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_STREAM] = (int64_t)stream;
       p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_DRAW0] = (int64_t)c.ctr;
+      if (!ok) report_error(c, p, j);
+    }
+  }
+}
+
+// deferred init, second half: init_post with the batched evaluation of the
+// starting point (lp[j], j = chain), exactly as fsm_init_kernel would
+template <template <int, int> class F, int G, int E>
+__global__ void __launch_bounds__(kThreads) fsm_init_finish_kernel(Params p) {
+  Grp<G> grp;
+  const int gib = threadIdx.x / G;
+  const long long groups = (long long)gridDim.x * (kThreads / G);
+  for (long long j = (long long)blockIdx.x * (kThreads / G) + gib; j < p.st.m; j += groups) {
+    Core c;
+    core_load(c, p, j);
+    if (c.err_kind != FSMC_E_NONE) continue;
+    F<G, E> f;
+    f.load(p, j, grp);
+    bool ok = true;
+    if constexpr (F<G, E>::SHAPE != SHAPE_NESTED) {
+      f.init_pre();
+      const double lp = p.b_init_lp[j];
+      if (is_target_failure(lp)) {
+        set_error(c, FSMC_E_TARGET, 1);
+        ok = false;
+      } else {
+        ok = f.init_post(c, lp);
+      }
+    }
+    f.store(p, j, grp);
+    if (grp.lane == 0) {
+      core_store(c, p, j);
       if (!ok) report_error(c, p, j);
     }
   }
@@ -373,6 +407,12 @@ struct Launch {
     fsm_init_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p, ps, off, x0, jit);
     return cudaGetLastError();
   }
+  static cudaError_t init_finish(const Params& p, cudaStream_t s) {
+    long long groups = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
+    int blocks = (int)std::min<long long>(groups, 1 << 20);
+    fsm_init_finish_kernel<F, G, E><<<blocks, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+  }
   // a persistent chain-queue kernel with as many blocks as are co-resident
   template <class KF>
   static cudaError_t persistent(KF* kern, const Params& p, const LaunchCtx& lc, cudaStream_t s,
@@ -436,11 +476,12 @@ struct Launch {
   }
 };
 
-// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile, 7 advance with batched prior (5 windowed run and 6 draws: fam_drmh.cu).  TK: compile-time plugin (0 = run-time switch)
+// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile, 7 advance with batched prior, 8 deferred-init finish (5 windowed run and 6 draws: fam_drmh.cu).  TK: compile-time plugin (0 = run-time switch)
 template <template <int, int> class F, int G, int E, int TK = 0>
 cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, uint64_t ps,
                       long long off, const double* x0, double jit) {
   if (op == 0) return Launch<F, G, E, 0>::init(p, ps, off, x0, jit, s);
+  if (op == 8) return Launch<F, G, E, 0>::init_finish(p, s);
   if (op == 1) return Launch<F, G, E, TK>::run(p, lc, s);
   if (op == 3) return Launch<F, G, E, 0>::advance(p, lc, s);
   if (op == 4) return Launch<F, G, E, 0>::profile(p, lc, s);

@@ -160,3 +160,57 @@ class PriorTransform:
             if st != 0:
                 raise RuntimeError(f"cublasDtrmm failed ({st})")
         rows.copy_(out)
+
+
+# ----------------------------------------------------------- GP hyperparameters
+_LOG_2PI = 1.8378770664093453
+_FAILURE = torch.tensor([0x7ff80000dead0001], dtype=torch.int64).view(torch.float64)  # fsm_device.cuh
+
+
+class GPHyperEvaluator:
+    """Batched evaluator of the GP-hyperparameter target (targets.py:191-265)
+    for designs too large for the per-chain shared-memory plugin (the
+    paper's section 7.2 uses n = 414 observations).  Per round, for the k
+    requesting chains theta = (sigma, tau, lam):
+
+        K_j = tau_j^2 exp(-lam_j^2 D2) + (sigma_j^2 + jitter) I     [k, n, n]
+        L_j = chol(K_j),  alpha_j = K_j^-1 y,  lml_j = -y.alpha_j/2 - sum log diag L_j - n log(2 pi)/2
+
+    as batched fp64 factorizations (cuSOLVER through torch.linalg), tiled
+    over chains.  ``residual=True`` returns the marginal likelihood (the
+    elliptical kernel's residual log density); otherwise the N(0, I) prior
+    terms are added.  The gradient is the reference's trace form with
+    A = alpha alpha^T - K^-1.  A kernel matrix that is not positive definite
+    returns the plugin's TargetError payload for that chain."""
+
+    def __init__(self, d2, y, jitter: float, residual: bool, tile: int = 512):
+        self.d2 = torch.as_tensor(d2, dtype=torch.float64, device="cuda").contiguous()
+        self.y = torch.as_tensor(y, dtype=torch.float64, device="cuda").contiguous()
+        self.jitter, self.residual, self.tile = float(jitter), bool(residual), int(tile)
+        self.n = self.y.shape[0]
+
+    def __call__(self, theta, lp, g=None):
+        n, d2, y = self.n, self.d2, self.y
+        fail = _FAILURE.to(lp.device)
+        for a in range(0, theta.shape[0], self.tile):
+            th = theta[a:a + self.tile]
+            s, t, lam = th[:, 0], th[:, 1], th[:, 2]
+            E = torch.exp((-(lam * lam))[:, None, None] * d2)
+            K = (t * t)[:, None, None] * E
+            K.diagonal(dim1=1, dim2=2).add_((s * s + self.jitter)[:, None])
+            L, info = torch.linalg.cholesky_ex(K)
+            alpha = torch.cholesky_solve(y.expand(th.shape[0], n)[..., None], L)[..., 0]
+            logdet = 2.0 * torch.log(L.diagonal(dim1=1, dim2=2)).sum(-1)
+            out = -0.5 * (y * alpha).sum(-1) - 0.5 * logdet - 0.5 * n * _LOG_2PI
+            if not self.residual:
+                out = out - 0.5 * (th * th).sum(-1) - 1.5 * _LOG_2PI
+            bad = info != 0
+            lp[a:a + self.tile] = torch.where(bad, fail, out)
+            if g is not None:
+                A = alpha[:, :, None] * alpha[:, None, :] - torch.cholesky_inverse(L)
+                AE = A * E
+                gr = torch.stack([s * A.diagonal(dim1=1, dim2=2).sum(-1), t * AE.sum((1, 2)),
+                                  -lam * t * t * (AE * d2).sum((1, 2))], dim=1)
+                if not self.residual:
+                    gr = gr - th
+                g[a:a + self.tile] = gr

@@ -291,10 +291,24 @@ def init_batch(bundle, target, m: int, seed: int, x0=None, init_jitter: float = 
     if tuple(x0d.shape) != (d,):
         raise ValueError(f"x0 shape {tuple(x0d.shape)} does not match dim {d}")
     batch = ChainBatch(bundle, target, m, seed, parent_stream, chain_offset)
-    _lib.check(_lib.lib().fsmc_init(ctypes.byref(batch.kernel), ctypes.byref(target.struct()),
-                                    ctypes.byref(batch.struct()), parent_stream & ((1 << 64) - 1),
-                                    chain_offset, x0d.data_ptr(), float(init_jitter),
-                                    _lib.stream_ptr()), "fsmc_init")
+    lib = _lib.lib()
+    args = (ctypes.byref(batch.kernel), ctypes.byref(target.struct()), ctypes.byref(batch.struct()),
+            parent_stream & ((1 << 64) - 1), chain_offset, x0d.data_ptr(), float(init_jitter),
+            _lib.stream_ptr())
+    ev = None
+    if hasattr(target, "batched_evaluator") and bundle.family != _lib.NUTS:
+        ev = target.batched_evaluator(bundle.family)
+    if ev is None:
+        _lib.check(lib.fsmc_init(*args), "fsmc_init")
+    else:
+        # starting points evaluated in one batched call (fsmc_init_deferred/_finish)
+        _lib.check(lib.fsmc_init_deferred(*args), "fsmc_init_deferred")
+        X = batch.vec[:, 0, :].contiguous()
+        lp = torch.empty(m, dtype=torch.float64, device="cuda")
+        ev(X, lp, None)
+        _lib.check(lib.fsmc_init_finish(ctypes.byref(batch.kernel), ctypes.byref(target.struct()),
+                                        ctypes.byref(batch.struct()), lp.data_ptr(),
+                                        _lib.stream_ptr()), "fsmc_init_finish")
     err = batch.first_error()
     if err is not None:
         raise _cause(bundle, err[1], err[2])
@@ -395,7 +409,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     variant = _VARIANT_ID[step_variant]
 
     if evaluator is None and hasattr(target, "batched_evaluator"):
-        evaluator = target.batched_evaluator()
+        evaluator = target.batched_evaluator(bundle.family)
     if draw_window and (bundle.family != _lib.DRMH or evaluator is not None):
         raise ValueError("draw_window applies to the DRMH kernels without an evaluator")
     if prior_transform is not None:
@@ -604,7 +618,7 @@ def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
     rec = bundle.loop_states
     samples, loops, _, out = _outputs(n, m, d, len(rec), False)
     if evaluator is None and hasattr(target, "batched_evaluator"):
-        evaluator = target.batched_evaluator()
+        evaluator = target.batched_evaluator(bundle.family)
     stats = None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -654,7 +668,7 @@ def _lockstep_batched(bundle, target, batch, n, out, lanes, evaluator) -> dict:
     g = torch.empty((m, d), dtype=torch.float64, device="cuda") if grad else None
     req_chain = torch.empty(m, dtype=torch.int32, device="cuda")
     req_count = torch.zeros(1, dtype=torch.int32, device="cuda")
-    level = torch.zeros(2, dtype=torch.int64, device="cuda")
+    level = torch.zeros(3, dtype=torch.int64, device="cuda")
     lib = _lib.lib()
     kern, tgt = batch.kernel, target.struct()
     stats = {"rounds": 0, "evaluations": 0}
@@ -668,6 +682,8 @@ def _lockstep_batched(bundle, target, batch, n, out, lanes, evaluator) -> dict:
         k = int(req_count.item())
         if k == 0:
             return stats
+        if int(level[2].item()) == 0:   # only idle requests: the barrier opens, no evaluation
+            continue
         stats["rounds"] += 1
         stats["evaluations"] += k
         evaluator(theta[:k], lp[:k], None if g is None else g[:k])

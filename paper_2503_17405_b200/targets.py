@@ -124,6 +124,9 @@ class TargetModel:
         m = X.shape[0]
         lp = torch.empty(m, dtype=torch.float64, device="cuda")
         g = torch.empty_like(X) if grad else None
+        if hasattr(self, "batched_evaluator"):     # no per-chain plugin for this design
+            self.batched_evaluator(_lib.ESS if self.residual_only else 0)(X, lp, g)
+            return lp, g
         t = self.struct()
         fam = _lib.ESS if self.residual_only else 0
         _lib.check(_lib.lib().fsmc_target_eval(ctypes.byref(t), X.data_ptr(), m, lp.data_ptr(),
@@ -332,13 +335,19 @@ def _sq_dists(X: np.ndarray) -> np.ndarray:
     return d2
 
 
-def gp_hyperparameter_target(inputs, outputs, jitter: float = 1e-8) -> TargetModel:
+def gp_hyperparameter_target(inputs, outputs, jitter: float = 1e-8,
+                             evaluation: str = "auto") -> TargetModel:
     """Posterior over theta = (sigma, tau, lam) of a squared-exponential GP
     regression (targets.py:191-265): K = tau^2 exp(-lam^2 D2) + (sigma^2 +
     jitter) I, N(0, 1) priors, so the Gaussian-prior split has the identity
     factor and the marginal likelihood as residual.  Each evaluation factors
     the chain's own n x n kernel matrix in shared memory (one warp per chain);
-    the gradient adds W = L^-1 and the three trace terms."""
+    the gradient adds W = L^-1 and the three trace terms.
+
+    ``evaluation``: "plugin" (n <= 56), "batched" (every evaluation and the
+    starting points through ``dense.GPHyperEvaluator``: batched fp64
+    Cholesky factorizations across chains, any n) or "auto" (the plugin when
+    it fits)."""
     X = np.asarray(inputs, dtype=float)
     y = np.ascontiguousarray(np.asarray(outputs, dtype=float))
     if X.ndim != 2 or X.shape[0] < 2:
@@ -346,15 +355,30 @@ def gp_hyperparameter_target(inputs, outputs, jitter: float = 1e-8) -> TargetMod
     if y.shape != (X.shape[0],):
         raise TargetError(f"outputs shape {y.shape} does not match {X.shape[0]} rows")
     n = X.shape[0]
-    if n > GP_DEVICE_MAX_ROWS:
+    if evaluation not in ("auto", "plugin", "batched"):
+        raise ValueError("evaluation must be auto, plugin or batched")
+    if evaluation == "auto":
+        evaluation = "plugin" if n <= GP_DEVICE_MAX_ROWS else "batched"
+    if evaluation == "plugin" and n > GP_DEVICE_MAX_ROWS:
         raise TargetError(f"the per-chain GP plugin handles n <= {GP_DEVICE_MAX_ROWS} "
                           f"observations, got {n}")
     arrays = {"data": np.ascontiguousarray(_sq_dists(X)), "yvec": y}
+    batched = evaluation == "batched"
     common = dict(name=f"gp-hyper-n{n}", dim=3, kind=_lib.T_GP_HYPER, a=float(jitter),
-                  arrays=arrays, scratch=2 * n * n + 2 * n + 4,
+                  arrays=arrays, scratch=0 if batched else 2 * n * n + 2 * n + 4,
                   log_density_cost=(n / 50.0) ** 3)
     residual = TargetModel(**common, residual_only=True)
-    return TargetModel(**common, gaussian_prior=GaussianPriorDecomposition(np.eye(3), residual))
+    t = TargetModel(**common, gaussian_prior=GaussianPriorDecomposition(np.eye(3), residual))
+    if batched:
+        from .dense import GPHyperEvaluator
+
+        def batched_evaluator(family=None, _t=t):
+            dev = _t.device_arrays()
+            return GPHyperEvaluator(dev["data"], dev["yvec"], jitter,
+                                    residual=family == _lib.ESS)
+        t.batched_evaluator = batched_evaluator
+        residual.batched_evaluator = lambda family=None, _t=t: batched_evaluator(_lib.ESS)
+    return t
 
 
 def make_synthetic_gp_dataset(n: int = 50, p: int = 3, seed: int = GP_DATA_SEED,
