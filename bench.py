@@ -53,8 +53,8 @@ CONFIGS = {
                prior_transform="trmm"),
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; batched TF32 gradient evaluation across chains",
-               family="nuts", m=131072, n=8, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
-               batched="bf16-tc", n_lock=2),
+               family="nuts", m=131072, n=32, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
+               batched="bf16-tc"),
 }
 
 
@@ -359,8 +359,11 @@ def main():
                        "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel"),
             "kernel_ms": kms, "algorithmic_bytes": traffic_bytes,
             "note": "HBM carries samples, ledger rows, chain state and (windowed) the pre-drawn "
-                    "normals/uniforms, 16 B per draw; the run is fp64/integer issue-bound: see "
-                    "'compute' and profiles/"}
+                    "normals/uniforms, 16 B per draw (written by drmh_draws_kernel, read by "
+                    "fsm_window_kernel: a design choice, see frac_without_draws); the run is "
+                    "fp64/integer issue-bound: see 'compute' and profiles/"}
+    if draw_bytes:
+        roof["frac_without_draws"] = (st_bytes + out_bytes) / (kms / 1e3) / 1e9 / peaks["hbm_gbs"]
     if cfg["family"] == "drmh" and proposals:
         # executed fp64 flops per DRMH proposal (DFMA = 2), from ncu SASS counts of
         # this pair of kernels (profiles/r01b_c2_ncu.md); peak = measured DFMA rate
