@@ -49,6 +49,7 @@ HOST_HARNESS = r"""
 #include "prng.cuh"
 extern "C" double h_log(double x) { return fsmc::gl_log(x); }
 extern "C" double h_ndtri(double x) { return fsmc::ndtri(x); }
+extern "C" double h_softplus(double a) { return fsmc::softplus_neg(a); }
 extern "C" double h_normal(unsigned long long seed, unsigned long long stream,
                            unsigned long long ctr) {
   return fsmc::normal(fsmc::hash_seed_stream(seed, stream), ctr);
@@ -82,7 +83,7 @@ def host_math(tmp_path_factory):
     subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-mfma", "-std=c++17", "-fPIC",
                            "-shared", f"-I{csrc}", "-o", str(so), str(src)])
     h = ctypes.CDLL(str(so))
-    for f in ("h_log", "h_ndtri"):
+    for f in ("h_log", "h_ndtri", "h_softplus"):
         getattr(h, f).restype = ctypes.c_double
         getattr(h, f).argtypes = [ctypes.c_double]
     h.h_normal.restype = ctypes.c_double
@@ -90,6 +91,30 @@ def host_math(tmp_path_factory):
     h.h_log_mismatch.restype = ctypes.c_long
     h.h_log_mismatch.argtypes = [ctypes.c_long, ctypes.c_ulonglong]
     return h
+
+
+def test_branch_free_softplus_is_accurate(host_math):
+    """softplus_neg(a) = log1p(exp(-a)) (logistic likelihood, NUTS logaddexp)
+    within 2 ulp of the correctly rounded value over [0, 745] and at the
+    range ends."""
+    from fractions import Fraction  # noqa: F401  (exactness reference below is mpmath)
+    mpmath = pytest.importorskip("mpmath")
+    mpmath.mp.prec = 200
+    rng = np.random.default_rng(7)
+    a = np.concatenate([rng.uniform(0, 1, 3000), rng.uniform(0, 40, 3000),
+                        rng.exponential(3.0, 2000), rng.uniform(40, 745, 500),
+                        [0.0, 1e-300, 5e-324, 1e-17, 0.34657359027997264, 0.6931471805599453,
+                         1.0, 36.7, 37.5, 700.0, 709.0, 745.0]])
+    worst = 0.0
+    for v in a:
+        got = host_math.h_softplus(float(v))
+        ref = float(mpmath.log1p(mpmath.exp(-mpmath.mpf(float(v)))))
+        if v > 700:      # clamped at e^-700: the term is below any sum's resolution
+            assert 0.0 <= got <= 1e-303
+            continue
+        ulp = math.ulp(ref)
+        worst = max(worst, abs(got - ref) / ulp)
+    assert worst <= 2.0, worst
 
 
 def test_glibc_log_restatement_is_bit_exact(host_math):
