@@ -292,6 +292,21 @@ fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16
                                 double* lp, double* grad, void* stream_);
 const char* fsmc_logreg_tc_last_error(void);
 
+/* Batched GP-hyperparameter marginal likelihood (targets.py:191-265) for k
+ * requesting chains, theta [k][3] = (sigma, tau, lam): one CTA per chain, a
+ * left-looking blocked Cholesky of K = tau^2 exp(-lam^2 D2) + (sigma^2 +
+ * jitter) I formed on the fly from d2 [n][n], plus the forward solve and the
+ * log determinant.  lp[j] = the marginal likelihood (residual != 0, the
+ * elliptical kernel's residual) or the log density (+ the N(0, I) prior);
+ * a matrix that is not positive definite yields the plugin's TargetError
+ * payload.  work: work_slots x n x n doubles (one slot per concurrent CTA).
+ * Errors: fsmc_gp_last_error(). */
+size_t fsmc_gp_lml_smem_bytes(int64_t n);
+fsmc_status fsmc_gp_lml(const double* theta, int64_t k, const double* d2, const double* y, int64_t n,
+                        double jitter, int32_t residual, double* work, int64_t work_slots, double* lp,
+                        void* stream_);
+const char* fsmc_gp_last_error(void);
+
 /* Cross-chain diagnostic partials for effective_sample_size / R-hat
  * (analysis.py:336-418).  samples [n][m][dim]; uses rows burn..n-1.
  *   chain_mean [m][dim] (computed when lag0 == 0), acov [32][dim] = sum over chains of

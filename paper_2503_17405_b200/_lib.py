@@ -112,6 +112,10 @@ def lib():
     L.fsmc_init_finish.restype = S
     L.fsmc_init_finish.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                    ctypes.POINTER(State), _P, _P]
+    L.fsmc_gp_lml.restype = S
+    L.fsmc_gp_lml.argtypes = [_P, ctypes.c_int64, _P, _P, ctypes.c_int64, _D, ctypes.c_int32, _P,
+                              ctypes.c_int64, _P, _P]
+    L.fsmc_gp_last_error.restype = ctypes.c_char_p
     L.fsmc_advance_lockstep.restype = S
     L.fsmc_advance_lockstep.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                         ctypes.POINTER(State), ctypes.c_int64,

@@ -176,8 +176,9 @@ class GPHyperEvaluator:
         K_j = tau_j^2 exp(-lam_j^2 D2) + (sigma_j^2 + jitter) I     [k, n, n]
         L_j = chol(K_j),  alpha_j = K_j^-1 y,  lml_j = -y.alpha_j/2 - sum log diag L_j - n log(2 pi)/2
 
-    as batched fp64 factorizations (cuSOLVER through torch.linalg), tiled
-    over chains.  ``residual=True`` returns the marginal likelihood (the
+    by ``fsmc_gp_lml`` (csrc/gp_chol.cu: one CTA per chain, a left-looking
+    blocked Cholesky with K formed on the fly) for values, and by batched
+    fp64 factorizations (torch.linalg) where the gradient is needed.  ``residual=True`` returns the marginal likelihood (the
     elliptical kernel's residual log density); otherwise the N(0, I) prior
     terms are added.  The gradient is the reference's trace form with
     A = alpha alpha^T - K^-1.  A kernel matrix that is not positive definite
@@ -188,8 +189,32 @@ class GPHyperEvaluator:
         self.y = torch.as_tensor(y, dtype=torch.float64, device="cuda").contiguous()
         self.jitter, self.residual, self.tile = float(jitter), bool(residual), int(tile)
         self.n = self.y.shape[0]
+        self.slots = torch.cuda.get_device_properties(self.d2.device).multi_processor_count
+        self.work = None
+        self.min_kernel_rows = 16
 
     def __call__(self, theta, lp, g=None):
+        # value only, enough requests to fill the SMs: the hand-written kernel
+        # (csrc/gp_chol.cu, one CTA per chain); a handful of requests runs
+        # faster through the library factorization, which spreads one matrix
+        # over the whole GPU
+        if g is None and theta.shape[0] >= self.min_kernel_rows:
+            if self.work is None:
+                self.work = torch.empty((self.slots, self.n, self.n), dtype=torch.float64,
+                                        device=self.d2.device)
+            theta = theta.contiguous()
+            st = _lib.lib().fsmc_gp_lml(theta.data_ptr(), theta.shape[0], self.d2.data_ptr(),
+                                        self.y.data_ptr(), self.n, self.jitter, int(self.residual),
+                                        self.work.data_ptr(), self.slots, lp.data_ptr(),
+                                        _lib.stream_ptr())
+            if st != 0:
+                raise _lib.EngineError(_lib.lib().fsmc_gp_last_error().decode())
+            return
+        self.torch_eval(theta, lp, g)
+
+    def torch_eval(self, theta, lp, g=None):
+        """Value (and gradient) through torch.linalg's batched factorizations
+        (the gradient path: it needs K^-1 for the trace terms)."""
         n, d2, y = self.n, self.d2, self.y
         fail = _FAILURE.to(lp.device)
         for a in range(0, theta.shape[0], self.tile):
