@@ -43,7 +43,7 @@ FP64_FLOPS_PER_PROPOSAL = 976.0
 CONFIGS = {
     "c2": dict(workload="C2: DRMH FSM, correlated MoG d=10 (rho=0.9, modes -3/0/3), M=100, "
                         "scale=0.1, bundled", family="drmh", m=65536, n=1000, d=10,
-               variant="bundled", m_cpu=256, draw_window=2200),
+               variant="bundled", m_cpu=256, draw_window=2200, draw_parts=4),
     "c1": dict(workload="C1: elliptical slice FSM, conjugate Gaussian-likelihood d=100, amortized",
                family="ess", m=128, n=1000, d=100, variant="amortized", m_cpu=32),
     "c3": dict(workload="C3: NUTS FSM, equicorrelated Gaussian d=100 rho=0.99, eps=0.05, depth 10",
@@ -189,6 +189,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--draw-window", type=int, default=-1,
                     help="DRMH pre-drawn window in draws (0: inline generator; -1: config default)")
+    ap.add_argument("--draw-parts", type=int, default=0,
+                    help="DRMH windows: 1 or 2 chain halves overlapped on two streams (0: config)")
     ap.add_argument("--prior", default="", choices=["", "none", "trmm", "gemm", "device"],
                     help="ESS dense prior: batched nu = L eps per round (default: config's)")
     args = ap.parse_args()
@@ -199,6 +201,8 @@ def main():
         cfg["n"] = args.n
     if args.draw_window >= 0:
         cfg["draw_window"] = args.draw_window
+    if args.draw_parts:
+        cfg["draw_parts"] = args.draw_parts
     if args.prior:
         cfg["prior_transform"] = None if args.prior == "none" else args.prior
     rank = int(os.environ.get("RANK", 0))
@@ -246,7 +250,8 @@ def main():
         return fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
                                   output="torch", surplus=False, lanes=args.lanes,
                                   evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
-                                  prior_transform=cfg.get("prior_transform"), _timing=timing)
+                                  prior_transform=cfg.get("prior_transform"),
+                                  draw_parts=cfg.get("draw_parts", 1), _timing=timing)
 
     held = None
     for s in range(args.warmup):
@@ -327,7 +332,8 @@ def main():
         smp, _ = fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
                                     output="torch", surplus=False, lanes=args.lanes,
                                     evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
-                                    prior_transform=cfg.get("prior_transform"))
+                                    prior_transform=cfg.get("prior_transform"),
+                                    draw_parts=cfg.get("draw_parts", 1))
         if has_ess:
             _ = fm.effective_sample_size(smp, burn=burn).pooled
         else:

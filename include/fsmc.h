@@ -185,6 +185,16 @@ fsmc_status fsmc_run_windowed(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
                               const fsmc_outputs* out, int64_t window, double* draws, int32_t lanes,
                               void* stream_);
 
+/* fsmc_run_windowed with the chains in `parts` (1..4) contiguous parts, each
+ * alternating its draw-generation and window kernels on its own stream
+ * (internal streams, joined back to stream_ before returning), so the parts'
+ * kernels fill each other's kernel tails and launch gaps.  Results are
+ * identical for any parts. */
+fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                      int32_t variant, const int32_t* order, int64_t tick_limit,
+                                      int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
+                                      int32_t lanes, int32_t parts, void* stream_);
+
 /* Replaces measure_block_costs' timing loop (lockstep.py:454-498): runs every
  * chain with the plain executor up to tick_limit like fsmc_run (mode 1) and
  * adds per-state clock64() cycles to cycles[16] (device, zeroed by the

@@ -137,6 +137,8 @@ def lib():
                                     ctypes.POINTER(State), ctypes.c_int64, ctypes.c_int32,
                                     ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, ctypes.c_int32,
                                     ctypes.POINTER(Outputs), ctypes.c_int64, _P, ctypes.c_int32, _P]
+    L.fsmc_run_windowed_overlap.restype = S
+    L.fsmc_run_windowed_overlap.argtypes = list(L.fsmc_run_windowed.argtypes[:-1]) + [ctypes.c_int32, _P]
     L.fsmc_profile_blocks.restype = S
     L.fsmc_profile_blocks.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                       ctypes.POINTER(State), ctypes.c_int64, _P, _P]

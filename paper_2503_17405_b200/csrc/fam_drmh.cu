@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
   const unsigned lt = (1u << lane) - 1u;
   const int step = 32 % per;             // phase advance between a lane's slots
   const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
-  for (long long j = (long long)blockIdx.x * nw + wid; j < p.st.m; j += (long long)gridDim.x * nw) {
+  for (long long j = p.j_lo + (long long)blockIdx.x * nw + wid; j < p.j_hi; j += (long long)gridDim.x * nw) {
     const int64_t* q = p.st.ints + (size_t)j * FSMC_NINT;
     if (q[FSMC_I_ERR_KIND] != FSMC_E_NONE || q[FSMC_I_COUNT] >= n_stop || q[FSMC_I_TICK] >= p.tick_limit)
       continue;
@@ -67,8 +67,9 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
 
 static cudaError_t launch_drmh_draws(const Params& p, int num_sms, cudaStream_t s) {
   const int threads = 256, nw = threads / 32;
-  long long need = (p.st.m + nw - 1) / nw;
-  int blocks = (int)std::min<long long>(need, (long long)num_sms * 8);
+  long long need = (p.j_hi - p.j_lo + nw - 1) / nw;
+  const int per_sm = p.draw_blocks_per_sm > 0 ? p.draw_blocks_per_sm : 8;
+  int blocks = (int)std::max<long long>(1, std::min<long long>(need, (long long)num_sms * per_sm));
   drmh_draws_kernel<<<blocks, threads, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -550,6 +551,14 @@ fsmc_status fsmc_run_windowed(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
                               int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
                               const fsmc_outputs* out, int64_t window, double* draws, int32_t lanes,
                               void* stream_) {
+  return fsmc_run_windowed_overlap(k, t, st, n, variant, order, tick_limit, mode, out, window, draws, lanes,
+                                   1, stream_);
+}
+
+fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                      int32_t variant, const int32_t* order, int64_t tick_limit,
+                                      int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
+                                      int32_t lanes, int32_t parts, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->family != FSMC_DRMH) return fail(FSMC_ERR_UNSUPPORTED, "pre-drawn windows are for the DRMH kernels");
@@ -577,21 +586,70 @@ fsmc_status fsmc_run_windowed(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
   }
   p.draws = draws;
   p.window = window;
+  constexpr int kMaxParts = 4;
+  if (parts < 1 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 1..4");
+  if (st->m < parts) parts = 1;
   cudaStream_t cs = (cudaStream_t)stream_;
   unsigned* w = scratch().words;
-  p.next_chain = w;
-  p.unfinished = w + 8;
-  const int kCheck = 4;   // rounds between reads of the unfinished count
+  // parts > 1: the chains in contiguous parts, each alternating its draw
+  // generation and window kernels on its own stream, so one part's kernels
+  // fill the SMs another part's kernel tail and launch gaps leave idle
+  static cudaStream_t side[kMaxParts] = {};
+  static cudaEvent_t ev_fork = nullptr, ev_join[kMaxParts] = {};
+  if (parts > 1 && !side[1]) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    for (int h = 1; h < kMaxParts; h++) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&side[h], cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&ev_join[h], cudaEventDisableTiming));
+    }
+  }
+  static int draw_bps = -1;   // draws-kernel blocks per SM (FSMC_DRAW_BLOCKS_PER_SM; 0 = fill)
+  if (draw_bps < 0) {
+    const char* e = getenv("FSMC_DRAW_BLOCKS_PER_SM");
+    draw_bps = e ? atoi(e) : 0;
+    if (draw_bps < 0) draw_bps = 0;
+  }
+  Params ph[kMaxParts];
+  cudaStream_t sh[kMaxParts];
+  for (int h = 0; h < parts; h++) {
+    ph[h] = p;
+    ph[h].j_lo = st->m * h / parts;
+    ph[h].j_hi = st->m * (h + 1) / parts;
+    ph[h].next_chain = w + 16 * h;
+    ph[h].unfinished = w + 16 * h + 8;
+    ph[h].draw_blocks_per_sm = draw_bps;
+    sh[h] = h == 0 ? cs : side[h];
+  }
+  if (parts > 1) {
+    CUDA_TRY(cudaEventRecord(ev_fork, cs));
+    for (int h = 1; h < parts; h++) CUDA_TRY(cudaStreamWaitEvent(sh[h], ev_fork, 0));
+  }
+  const int kCheck = 4;   // rounds between reads of the unfinished counts
+  unsigned left[kMaxParts] = {1, 1, 1, 1};
   for (long long r = 0;; r++) {
-    CUDA_TRY(dispatch_family(6, ge, p, cs));
-    CUDA_TRY(cudaMemsetAsync(w, 0, sizeof(unsigned), cs));
-    CUDA_TRY(cudaMemsetAsync(p.unfinished, 0, sizeof(unsigned), cs));
-    CUDA_TRY(dispatch_family(5, ge, p, cs));
+    for (int h = 0; h < parts; h++) {
+      if (!left[h]) continue;
+      CUDA_TRY(dispatch_family(6, ge, ph[h], sh[h]));
+      CUDA_TRY(cudaMemsetAsync(ph[h].next_chain, 0, sizeof(unsigned), sh[h]));
+      CUDA_TRY(cudaMemsetAsync(ph[h].unfinished, 0, sizeof(unsigned), sh[h]));
+      CUDA_TRY(dispatch_family(5, ge, ph[h], sh[h]));
+    }
     if (r % kCheck == kCheck - 1) {
-      unsigned left = 0;
-      CUDA_TRY(cudaMemcpyAsync(&left, p.unfinished, sizeof(unsigned), cudaMemcpyDeviceToHost, cs));
-      CUDA_TRY(cudaStreamSynchronize(cs));
-      if (!left) break;
+      for (int h = 0; h < parts; h++)
+        if (left[h])
+          CUDA_TRY(cudaMemcpyAsync(&left[h], ph[h].unfinished, sizeof(unsigned), cudaMemcpyDeviceToHost, sh[h]));
+      bool any = false;
+      for (int h = 0; h < parts; h++) {
+        CUDA_TRY(cudaStreamSynchronize(sh[h]));
+        any = any || left[h];
+      }
+      if (!any) break;
+    }
+  }
+  if (parts > 1) {
+    for (int h = 1; h < parts; h++) {
+      CUDA_TRY(cudaEventRecord(ev_join[h], sh[h]));
+      CUDA_TRY(cudaStreamWaitEvent(cs, ev_join[h], 0));
     }
   }
   return FSMC_OK;

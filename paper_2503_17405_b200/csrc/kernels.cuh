@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_window_kernel(P
   while (true) {
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
-    j = grp.bcast_ll(j, 0);
-    if (j >= p.st.m) break;
+    j = p.j_lo + grp.bcast_ll(j, 0);
+    if (j >= p.j_hi) break;
     Core c;
     core_load(c, p, j);
     c.ws = ws;
@@ -416,7 +416,7 @@ struct Launch {
   // a persistent chain-queue kernel with as many blocks as are co-resident
   template <class KF>
   static cudaError_t persistent(KF* kern, const Params& p, const LaunchCtx& lc, cudaStream_t s,
-                                size_t sm_bytes = 0) {
+                                size_t sm_bytes = 0, long long chains = -1) {
     const size_t sb = sm_bytes ? sm_bytes : smem(p);
     int occ = 0;
     cudaError_t e = allow_smem(kern, sb);
@@ -424,8 +424,9 @@ struct Launch {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, sb);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
-    long long need = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
-    int blocks = (int)std::min<long long>(need, (long long)occ * lc.num_sms);
+    if (chains < 0) chains = p.st.m;
+    long long need = (chains + (kThreads / G) - 1) / (kThreads / G);
+    int blocks = (int)std::max<long long>(1, std::min<long long>(need, (long long)occ * lc.num_sms));
     kern<<<blocks, kThreads, sb, s>>>(p);
     return cudaGetLastError();
   }
@@ -443,8 +444,8 @@ struct Launch {
   static cudaError_t window(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     const size_t sb = std::max<size_t>(8, (size_t)(kThreads / G) * group_doubles(p.t) * sizeof(double));
     if constexpr (TK != 0)
-      if (unrolled(p)) return persistent(fsm_window_kernel<F, G, E, TK, 1>, p, lc, s, sb);
-    return persistent(fsm_window_kernel<F, G, E, TK, 0>, p, lc, s, sb);
+      if (unrolled(p)) return persistent(fsm_window_kernel<F, G, E, TK, 1>, p, lc, s, sb, p.j_hi - p.j_lo);
+    return persistent(fsm_window_kernel<F, G, E, TK, 0>, p, lc, s, sb, p.j_hi - p.j_lo);
   }
   static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     return persistent(fsm_advance_kernel<F, G, E>, p, lc, s);

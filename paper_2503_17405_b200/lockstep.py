@@ -355,7 +355,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     bundled_order: tuple | None = None, record_sample_ticks: bool = False,
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
                     lanes: int = 0, evaluator=None, draw_window: int = 0,
-                    prior_transform=None, _timing: dict | None = None):
+                    prior_transform=None, draw_parts: int = 1, _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
@@ -384,6 +384,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     ``draw_window`` (DRMH kernels): generate each chain's next ``draw_window``
     PRNG draws in a separate full-occupancy kernel and let the step kernel
     read them (``fsmc_run_windowed``); bit-identical to the inline draws.
+    ``draw_parts`` (1..4) splits the chains in parts whose generator and
+    step kernels overlap on their own streams (``fsmc_run_windowed_overlap``).
     """
     _validate_run_args(batch, n)
     bundle.check_target(target)
@@ -427,11 +429,12 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         draws = torch.empty(m * int(draw_window) + 32, dtype=torch.float64, device="cuda")
 
         def launch(mode, tick_limit):
-            _lib.check(lib.fsmc_run_windowed(ctypes.byref(kern), ctypes.byref(tgt),
-                                             ctypes.byref(batch.struct()), n, variant, ordv,
-                                             tick_limit, mode, ctypes.byref(out), int(draw_window),
-                                             draws.data_ptr(), lanes, _lib.stream_ptr()),
-                       "fsmc_run_windowed")
+            _lib.check(lib.fsmc_run_windowed_overlap(ctypes.byref(kern), ctypes.byref(tgt),
+                                                     ctypes.byref(batch.struct()), n, variant, ordv,
+                                                     tick_limit, mode, ctypes.byref(out),
+                                                     int(draw_window), draws.data_ptr(), lanes,
+                                                     int(draw_parts), _lib.stream_ptr()),
+                       "fsmc_run_windowed_overlap")
     elif evaluator is None:
         def launch(mode, tick_limit):
             _lib.check(lib.fsmc_run(ctypes.byref(kern), ctypes.byref(tgt),
