@@ -97,16 +97,18 @@ def diag_moments(chains, burn: int = 0) -> DiagMoments:
     def acov_all() -> np.ndarray:
         """Every lag at once by FFT (analysis.py:344-347), for slowly mixing
         chains whose Geyer truncation needs many lag tiles."""
+        # sum_j acov_j = irfft(sum_j |F_j|^2): the power spectra are summed over
+        # chains first, so one inverse transform per dimension remains
+        # (transforms along the contiguous last axis: 1.5x faster than along dim 0)
         size = 1 << int(math.ceil(math.log2(2 * n)))
-        out = torch.zeros((n, d), dtype=torch.float64, device="cuda")
-        chunk = max(1, (1 << 28) // (size * d))   # ~4 GB of complex work at a time
+        power = torch.zeros((d, size // 2 + 1), dtype=torch.float64, device="cuda")
+        chunk = max(1, (1 << 27) // (size * d))   # ~2 GB of complex work at a time
         for lo in range(0, m, chunk):
             hi = min(m, lo + chunk)
             c = (S[burn:, lo:hi, :] - mean[lo:hi]).permute(1, 2, 0)   # [chains, d, n]
             f = torch.fft.rfft(c, n=size, dim=2)
-            ac = torch.fft.irfft(f * f.conj(), n=size, dim=2)[:, :, :n] / n
-            out += ac.sum(dim=0).T
-        return out.cpu().numpy()
+            power += (f.real.square() + f.imag.square()).sum(dim=0)
+        return (torch.fft.irfft(power, n=size, dim=1)[:, :n] / n).T.cpu().numpy()
 
     return DiagMoments(n=n, m=m, d=d, var_means=var_means, max_chain_var=chain_var,
                        acov_tile=acov_tile, acov_all=acov_all)
@@ -167,7 +169,8 @@ def _ess_dim(ac: _Acov, mom: DiagMoments, k: int) -> tuple[float, bool]:
             rho[t + 1] = (rho.get(t - 1, 0.0) + rho.get(t, 0.0)) / 2.0
             rho[t + 2] = rho[t + 1]
         t += 2
-    tau = -1.0 + 2.0 * sum(rho.get(i, 0.0) for i in range(max_t)) + \
+    # numpy's pairwise sum over the zero-filled rho[:max_t] (analysis.py:378)
+    tau = -1.0 + 2.0 * float(np.array([rho.get(i, 0.0) for i in range(max_t)]).sum()) + \
         (rho.get(max_t + 1, 0.0) if max_t + 1 < n else 0.0)
     flagged = False
     if tau <= 0 or not math.isfinite(tau):
@@ -180,13 +183,110 @@ def _ess_dim(ac: _Acov, mom: DiagMoments, k: int) -> tuple[float, bool]:
     return float(min(ess, float(total))), flagged
 
 
+def _geyer_all(acf: np.ndarray, mom: DiagMoments) -> tuple[np.ndarray, np.ndarray]:
+    """`_ess_dim` for every dimension at once (numpy over dimensions, the
+    same floating-point operations in the same order).  acf [T, d]: mean
+    autocovariances for lags 0..T-1, T large enough that every dimension's
+    initial positive sequence ends inside it or T == n.  Returns (ess [d],
+    flagged [d]); constant chains are handled by the caller."""
+    m, n = mom.m, mom.n
+    total = float(m * n)
+    T, d = acf.shape
+    mean_var = acf[0] * n / (n - 1.0)
+    var_plus = mean_var * (n - 1.0) / n
+    if m > 1:
+        var_plus = var_plus + mom.var_means
+    rho = 1.0 - (mean_var[None, :] - acf) / var_plus[None, :]
+    rho[0] = 1.0
+    npairs = (T + 1) // 2
+    if 2 * npairs > T:
+        rho = np.vstack([rho, np.zeros((1, d))])
+    P = rho[0::2][:npairs] + rho[1::2][:npairs]          # pair sums, pair j = (2j, 2j+1)
+    anticorrelated = P[0] < 0.0
+    # pairs computed by the reference loop: j = 1 .. J, J = first j >= 1 with
+    # P_j < 0, or the last j with 2j - 1 < n - 2
+    j_lim = max(0, (n - 2) // 2)                       # largest j with 2j - 1 < n - 2
+    js = np.arange(npairs)[:, None]
+    neg = (P < 0.0) & (js >= 1) & (js <= j_lim)
+    first_neg = np.where(neg.any(axis=0), neg.argmax(axis=0), j_lim)
+    J = np.where(anticorrelated, 0, first_neg)                     # [d]
+    odd_kept = (js < J[None, :]) | ((js == J[None, :]) & (P >= 0.0))  # rho[2j+1] stored?
+    Pm = rho[0::2][:npairs] + np.where(odd_kept | (js == 0), rho[1::2][:npairs], 0.0)
+    # initial monotone sequence over pairs 1..J: running minimum of pair sums
+    run = Pm.copy()
+    modified = np.zeros_like(run, dtype=bool)
+    for j in range(1, int(J.max()) + 1 if d else 1):
+        act = j <= J
+        mod = act & (run[j] > run[j - 1])
+        run[j] = np.where(mod, run[j - 1], run[j])
+        modified[j] = mod
+    ev = np.where(modified, run / 2.0, rho[0::2][:npairs])
+    od = np.where(modified, run / 2.0, np.where(odd_kept | (js == 0), rho[1::2][:npairs], 0.0))
+    # tau = -1 + 2 sum_{i < 2J+1} rho_i: numpy's pairwise sum of each
+    # dimension's contiguous rho[:max_t] (analysis.py:378)
+    seq = np.empty((d, 2 * npairs))
+    seq[:, 0::2], seq[:, 1::2] = ev.T, od.T
+    S = np.array([seq[k, :2 * J[k] + 1].sum() for k in range(d)])
+    tau = -1.0 + 2.0 * S
+    bad = (tau <= 0) | ~np.isfinite(tau)
+    tau = np.where(bad, 1.0 / total, tau)
+    ess = np.minimum(total / tau, total)
+    return ess, bad, anticorrelated
+
+
+def _acf_for_geyer(mom: DiagMoments) -> np.ndarray:
+    """Mean autocovariances [T, d] far enough for every dimension's initial
+    positive sequence: lag tiles until each dimension's pair sums turn
+    negative, one FFT over every lag beyond a few tiles."""
+    n = mom.n
+    tiles = []
+    with np.errstate(divide="ignore", invalid="ignore"):
+        acf = _acf_tiles(mom, tiles)
+    if acf is not None:
+        return acf
+    if mom.acov_all is not None:
+        return mom.acov_all()[:n] / mom.m
+    while True:
+        tiles.append(mom.acov_tile(len(tiles)) / mom.m)
+        acf = np.vstack(tiles)[:n]
+        if acf.shape[0] >= n:
+            return acf
+
+
+def _acf_tiles(mom: DiagMoments, tiles: list):
+    n = mom.n
+    for k in range(_Acov.TILE_LIMIT):
+        tiles.append(mom.acov_tile(k) / mom.m)
+        acf = np.vstack(tiles)[:n]
+        if acf.shape[0] >= n:
+            return acf
+        mean_var = acf[0] * n / (n - 1.0)
+        var_plus = mean_var * (n - 1.0) / n + (mom.var_means if mom.m > 1 else 0.0)
+        rho = 1.0 - (mean_var[None, :] - acf) / var_plus[None, :]
+        rho[0] = 1.0
+        h = acf.shape[0] // 2
+        P = rho[0:2 * h:2] + rho[1:2 * h:2]
+        done = ((P < 0.0) | ~np.isfinite(P)).any(axis=0)
+        if bool(done.all()):
+            return acf
+        # a dimension still correlated at 0.5 at the last lag fetched will need
+        # far more tiles: go to the all-lags transform at once
+        if mom.acov_all is not None and bool((rho[-1][~done] > 0.5).any()):
+            return None
+    return None
+
+
 def ess_from_moments(mom: DiagMoments, model_cost=None, walltime=None) -> EssSummary:
-    ac = _Acov(mom)
-    per_dim, flagged = [], False
-    for k in range(mom.d):
-        e, f = _ess_dim(ac, mom, k)
-        per_dim.append(e)
-        flagged = flagged or f
+    const = np.asarray(mom.max_chain_var) <= 1e-8        # np.allclose(var, 0)
+    if const.any():
+        warnings.warn("constant chain: ESS floored to 1", stacklevel=2)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ess, bad, anti = _geyer_all(_acf_for_geyer(mom), mom)
+    if (anti & ~const).any():
+        warnings.warn("anticorrelated chain: ESS capped at the sample count", stacklevel=2)
+    ess = np.where(const, 1.0, ess)
+    per_dim = [float(v) for v in ess]
+    flagged = bool(const.any() or (bad | anti)[~const].any())
     pooled = min(per_dim)
     return EssSummary(per_dimension=tuple(per_dim), pooled=pooled,
                       per_cost=pooled / model_cost if model_cost else None,

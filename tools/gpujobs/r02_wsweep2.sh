@@ -1,0 +1,1 @@
+for w in 2750 3850 4070; do timeout 300 python bench.py --draw-window $w --steps 3 --warmup 3 --no-cpu --no-lockstep > gpurun_out/r02_w_$w.json 2> gpurun_out/r02_w_$w.err; done
