@@ -17,7 +17,7 @@
 // X and X^T stages have separate full/empty barriers: an X stage is released
 // as soon as the first product has read it, so X loads run ahead of the
 // epilogue while X^T (needed two tiles later) streams in behind it.
-//   warps 2 .. 2+4*EPI_SPLIT-1  epilogue: TMEM lane quadrant (warp % 4) x a
+//   warps 2 .. 2+4*EPI_SPLIT-1  epilogue (16 warps): TMEM lane quadrant (warp % 4) x a
 //              column slice, one chain row per thread; sigmoid / softplus on
 //              MUFU ex2, rcp and lg2
 // S is double-buffered in TMEM so the epilogue of tile i overlaps MMA1 of i+1.
@@ -36,7 +36,7 @@ namespace {
 constexpr int BM = 128;       // chains per CTA (MMA M, TMEM lanes)
 constexpr int BN = 64;        // design rows per tile (MMA1 N, MMA2 K)
 constexpr int DF = 256;       // features (MMA1 K, MMA2 N)
-constexpr int EPI_SPLIT = 2;                 // epilogue warps per TMEM lane quadrant
+constexpr int EPI_SPLIT = 4;                 // epilogue warps per TMEM lane quadrant
 constexpr int N_EPI = 128 * EPI_SPLIT;        // epilogue threads
 constexpr int COLS = BN / EPI_SPLIT;          // S columns per epilogue thread
 constexpr int W_XT = 2 + N_EPI / 32;          // warp index of the X^T producer
@@ -248,30 +248,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar(B_SEMPTY0 + s));
-      // R = sigmoid(z);  sp += log(1 + e^z) = max(z, 0) + log1p(e^-|z|)
+      // R = sigmoid(z) = 1 / (1 + e^-z);  sp += log(1 + e^z) = z + ln(1 + e^-z).
+      // One exponential shared by both (z clamped at -87 keeps e^-z finite in
+      // fp32; below that softplus < 1e-37), no sign select: 7 instructions
+      // per element, the epilogue being issue-bound.  The validity test
+      // (design rows past N) only runs on the last tile.
       uint32_t packed[COLS / 2];
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
       const long long r0 = (long long)i * BN + half * COLS;
-      const int valid = r0 + COLS <= N ? COLS : (int)(N > r0 ? N - r0 : 0);  // last tile only
+      const int valid = r0 + COLS <= N ? COLS : (int)(N > r0 ? N - r0 : 0);
+      auto element = [&](float zz, float& sig) -> float {
+        const float zc = fmaxf(zz, -87.0f);
+        float en, l2;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(en) : "f"(-1.4426950408889634f * zc));
+        const float ope = 1.0f + en;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(sig) : "f"(ope));
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(ope));
+        return fmaf(0.6931471805599453f, l2, zc);
+      };
+      if (valid == COLS) {
 #pragma unroll
-      for (int c = 0; c < COLS; c += 2) {
-        float rv[2];
+        for (int c = 0; c < COLS; c += 2) {
+          float rv[2];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const float zz = z[c + h];
-          float e;
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * fabsf(zz)));
-          const float ope = 1.0f + e;
-          float inv, l2;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(ope));
-          asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(ope));   // log1p(e) = ln2 log2(1+e)
-          const float sp = fmaf(0.6931471805599453f, l2, fmaxf(zz, 0.0f));
-          const bool ok = (c + h) < valid;
-          acc[(c + h) & 3] += ok ? sp : 0.0f;
-          rv[h] = zz >= 0.0f ? inv : e * inv;   // rows past N have x = 0: no G term
+          for (int h = 0; h < 2; h++) acc[(c + h) & 3] += element(z[c + h], rv[h]);
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(rv[0], rv[1]);
+          packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(rv[0], rv[1]);
-        packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+      } else {
+#pragma unroll
+        for (int c = 0; c < COLS; c += 2) {
+          float rv[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const float sp = element(z[c + h], rv[h]);
+            acc[(c + h) & 3] += (c + h) < valid ? sp : 0.0f;   // rows past N have x = 0: no G term
+          }
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(rv[0], rv[1]);
+          packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+        }
       }
       lp_acc += (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
       mbar_wait(bar(B_REMPTY0 + s), ((i >> 1) & 1) ^ 1);
