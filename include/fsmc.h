@@ -309,9 +309,11 @@ const char* fsmc_logreg_tc_last_error(void);
  * log determinant.  lp[j] = the marginal likelihood (residual != 0, the
  * elliptical kernel's residual) or the log density (+ the N(0, I) prior);
  * a matrix that is not positive definite yields the plugin's TargetError
- * payload.  work: work_slots x n x n doubles (one slot per concurrent CTA).
+ * payload.  work: work_slots x n x n doubles (one slot per concurrent CTA);
+ * n <= fsmc_gp_lml_max_rows().
  * Errors: fsmc_gp_last_error(). */
 size_t fsmc_gp_lml_smem_bytes(int64_t n);
+int64_t fsmc_gp_lml_max_rows(void);   /* n limit of fsmc_gp_lml (shared memory) */
 fsmc_status fsmc_gp_lml(const double* theta, int64_t k, const double* d2, const double* y, int64_t n,
                         double jitter, int32_t residual, double* work, int64_t work_slots, double* lp,
                         void* stream_);

@@ -188,6 +188,12 @@ const char* fsmc_gp_last_error(void) { return g_err.c_str(); }
 
 size_t fsmc_gp_lml_smem_bytes(int64_t n) { return (size_t)((n * LDC) + NB * LDC + n + 4) * sizeof(double); }
 
+int64_t fsmc_gp_lml_max_rows(void) {   // the block column and the staged rows fit in 227 KB
+  int64_t n = 2;
+  while (fsmc_gp_lml_smem_bytes(n + 1) <= 227 * 1024) n++;
+  return n;
+}
+
 fsmc_status fsmc_gp_lml(const double* theta, int64_t k, const double* d2, const double* y, int64_t n,
                         double jitter, int32_t residual, double* work, int64_t work_slots, double* lp,
                         void* stream_) {
@@ -197,7 +203,7 @@ fsmc_status fsmc_gp_lml(const double* theta, int64_t k, const double* d2, const 
   }
   if (k == 0) return FSMC_OK;
   const size_t sb = fsmc_gp_lml_smem_bytes(n);
-  if (sb > 227 * 1024) {
+  if (n > fsmc_gp_lml_max_rows()) {
     g_err = "gp_lml: n too large for the shared-memory block column";
     return FSMC_ERR_UNSUPPORTED;
   }

@@ -198,7 +198,8 @@ class GPHyperEvaluator:
         # (csrc/gp_chol.cu, one CTA per chain); a handful of requests runs
         # faster through the library factorization, which spreads one matrix
         # over the whole GPU
-        if g is None and theta.shape[0] >= self.min_kernel_rows:
+        if g is None and theta.shape[0] >= self.min_kernel_rows and \
+                self.n <= _lib.lib().fsmc_gp_lml_max_rows():
             if self.work is None:
                 self.work = torch.empty((self.slots, self.n, self.n), dtype=torch.float64,
                                         device=self.d2.device)
