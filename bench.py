@@ -370,6 +370,15 @@ def main():
                     "fp64/integer issue-bound: see 'compute' and profiles/"}
     if draw_bytes:
         roof["frac_without_draws"] = (st_bytes + out_bytes) / (kms / 1e3) / 1e9 / peaks["hbm_gbs"]
+        tp = os.path.join(ROOT, "profiles", "r02_c2_traffic.json")
+        if os.path.exists(tp) and cfg.get("draw_window") == 3300:
+            # ncu DRAM bytes of one generator + window launch pair (draws + 4%:
+            # state and samples), scaled to this run by its draw bytes
+            t = json.load(open(tp))
+            roof["traffic"] = draw_bytes * t["measured_over_draw_bytes"]
+            roof["traffic_source"] = "profiles/r02_c2_traffic.json (per launch pair: %.0f MB measured, "\
+                "%.0f MB of draws)" % (t["measured_per_launch_pair"] / 1e6,
+                                      t["algorithmic_draw_bytes_per_launch_pair"] / 1e6)
     if cfg["family"] == "drmh" and proposals:
         # executed fp64 flops per DRMH proposal (DFMA = 2), from ncu SASS counts of
         # this pair of kernels (profiles/r01b_c2_ncu.md); peak = measured DFMA rate
