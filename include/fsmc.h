@@ -185,7 +185,7 @@ fsmc_status fsmc_run_windowed(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
                               const fsmc_outputs* out, int64_t window, double* draws, int32_t lanes,
                               void* stream_);
 
-/* fsmc_run_windowed with the chains in `parts` (1..4) contiguous parts, each
+/* fsmc_run_windowed with the chains in `parts` (1..8) contiguous parts, each
  * alternating its draw-generation and window kernels on its own stream
  * (internal streams, joined back to stream_ before returning), so the parts'
  * kernels fill each other's kernel tails and launch gaps.  Results are

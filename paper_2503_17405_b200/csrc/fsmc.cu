@@ -50,7 +50,7 @@ struct Scratch {
 };
 Scratch& scratch() {
   static Scratch s;
-  if (!s.words) cudaMalloc(&s.words, 64 * sizeof(unsigned));
+  if (!s.words) cudaMalloc(&s.words, 256 * sizeof(unsigned));
   return s;
 }
 }  // namespace
@@ -586,8 +586,8 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
   }
   p.draws = draws;
   p.window = window;
-  constexpr int kMaxParts = 4;
-  if (parts < 1 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 1..4");
+  constexpr int kMaxParts = 8;
+  if (parts < 1 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 1..8");
   if (st->m < parts) parts = 1;
   cudaStream_t cs = (cudaStream_t)stream_;
   unsigned* w = scratch().words;
@@ -625,7 +625,8 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
     for (int h = 1; h < parts; h++) CUDA_TRY(cudaStreamWaitEvent(sh[h], ev_fork, 0));
   }
   const int kCheck = 4;   // rounds between reads of the unfinished counts
-  unsigned left[kMaxParts] = {1, 1, 1, 1};
+  unsigned left[kMaxParts];
+  for (int h = 0; h < kMaxParts; h++) left[h] = 1;
   for (long long r = 0;; r++) {
     for (int h = 0; h < parts; h++) {
       if (!left[h]) continue;
