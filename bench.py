@@ -50,7 +50,7 @@ CONFIGS = {
                family="nuts", m=16384, n=1000, d=100, variant="bundled", m_cpu=16),
     "c4": dict(workload="C4: elliptical slice FSM, GP-classification latent d=1024 (f-space)",
                family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4,
-               prior_transform="trmm"),
+               prior_transform="trmm", prior_parts=3),
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; batched TF32 gradient evaluation across chains",
                family="nuts", m=131072, n=32, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
@@ -191,6 +191,8 @@ def main():
                     help="DRMH pre-drawn window in draws (0: inline generator; -1: config default)")
     ap.add_argument("--draw-parts", type=int, default=0,
                     help="DRMH windows: 1 or 2 chain halves overlapped on two streams (0: config)")
+    ap.add_argument("--prior-parts", type=int, default=0,
+                    help="ESS batched prior: chain parts overlapped on their own streams (0: config)")
     ap.add_argument("--prior", default="", choices=["", "none", "trmm", "gemm", "device"],
                     help="ESS dense prior: batched nu = L eps per round (default: config's)")
     args = ap.parse_args()
@@ -203,6 +205,8 @@ def main():
         cfg["draw_window"] = args.draw_window
     if args.draw_parts:
         cfg["draw_parts"] = args.draw_parts
+    if args.prior_parts:
+        cfg["prior_parts"] = args.prior_parts
     if args.prior:
         cfg["prior_transform"] = None if args.prior == "none" else args.prior
     rank = int(os.environ.get("RANK", 0))
@@ -251,7 +255,8 @@ def main():
                                   output="torch", surplus=False, lanes=args.lanes,
                                   evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
                                   prior_transform=cfg.get("prior_transform"),
-                                  draw_parts=cfg.get("draw_parts", 1), _timing=timing)
+                                  draw_parts=cfg.get("draw_parts", 1),
+                                  prior_parts=cfg.get("prior_parts", 1), _timing=timing)
 
     held = None
     for s in range(args.warmup):
@@ -333,7 +338,8 @@ def main():
                                     output="torch", surplus=False, lanes=args.lanes,
                                     evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
                                     prior_transform=cfg.get("prior_transform"),
-                                    draw_parts=cfg.get("draw_parts", 1))
+                                    draw_parts=cfg.get("draw_parts", 1),
+                                    prior_parts=cfg.get("prior_parts", 1))
         if has_ess:
             _ = fm.effective_sample_size(smp, burn=burn).pooled
         else:

@@ -275,6 +275,15 @@ fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_
                                const fsmc_outputs* out, double* nu, int32_t* req_chain,
                                int32_t* req_count, int32_t lanes, void* stream_);
 
+/* fsmc_advance_prior over the chains [j_lo, j_hi) only, with its own chain
+ * queue (part 0..7): the chains split in parts whose rounds run on their own
+ * streams, so one part's GEMM overlaps another part's advance kernel. */
+fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                    int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                                    const fsmc_outputs* out, double* nu, int32_t* req_chain,
+                                    int32_t* req_count, int32_t lanes, int64_t j_lo, int64_t j_hi,
+                                    int32_t part, void* stream_);
+
 /* nu[r][:] = L nu[r][:] in place for r < k (L = the target's dense prior
  * factor), each row summed in the sampling kernel's order: the bit-exact
  * prior transform for fsmc_advance_prior. */

@@ -127,6 +127,9 @@ def lib():
                                      ctypes.POINTER(State), ctypes.c_int64, ctypes.c_int32,
                                      ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, ctypes.c_int32,
                                      ctypes.POINTER(Outputs), _P, _P, _P, ctypes.c_int32, _P]
+    L.fsmc_advance_prior_part.restype = S
+    L.fsmc_advance_prior_part.argtypes = list(L.fsmc_advance_prior.argtypes[:-1]) + \
+        [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _P]
     L.fsmc_prior_apply.restype = S
     L.fsmc_prior_apply.argtypes = [ctypes.POINTER(Target), _P, ctypes.c_int64, _P]
     L.fsmc_lockstep_run.restype = S

@@ -441,7 +441,11 @@ static fsmc_status advance_common(int op, const fsmc_kernel* k, const fsmc_targe
                                   int32_t mode, const fsmc_outputs* out, const double* lp,
                                   const double* grad, double* theta, int32_t* req_chain,
                                   int32_t* req_count, int32_t lanes, void* stream_,
-                                  int64_t* level = nullptr) {
+                                  int64_t* level = nullptr, int64_t j_lo = 0, int64_t j_hi = -1,
+                                  int32_t part = -1) {
+  if (j_hi < 0) j_hi = st->m;
+  if (j_lo < 0 || j_lo > j_hi || j_hi > st->m || part >= 8)
+    return fail(FSMC_ERR_ARG, "advance: chain range or part out of bounds");
   if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
   GE ge;
   if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
@@ -474,7 +478,9 @@ static fsmc_status advance_common(int op, const fsmc_kernel* k, const fsmc_targe
     CUDA_TRY(cudaMemsetAsync(level + 1, 0x7f, sizeof(int64_t), cs));
     CUDA_TRY(cudaMemsetAsync(level + 2, 0, sizeof(int64_t), cs));
   }
-  p.next_chain = scratch().words;
+  p.j_lo = j_lo;
+  p.j_hi = j_hi;
+  p.next_chain = part < 0 ? scratch().words : scratch().words + 128 + 16 * part;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
   CUDA_TRY(cudaMemsetAsync(req_count, 0, sizeof(int32_t), cs));
   CUDA_TRY(dispatch_family(op, ge, p, cs));
@@ -517,6 +523,21 @@ fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_
     return fail(FSMC_ERR_ARG, "advance_prior needs nu, req_chain, req_count");
   return advance_common(7, k, t, st, n, variant, order, tick_limit, mode, out, nullptr, nullptr, nu,
                         req_chain, req_count, lanes, stream_);
+}
+
+fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                    int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                                    const fsmc_outputs* out, double* nu, int32_t* req_chain,
+                                    int32_t* req_count, int32_t lanes, int64_t j_lo, int64_t j_hi,
+                                    int32_t part, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (k->family != FSMC_ESS || t->prior_kind != FSMC_PRIOR_DENSE)
+    return fail(FSMC_ERR_UNSUPPORTED, "the batched prior transform is for the elliptical kernel with a dense prior");
+  if (!nu || !req_chain || !req_count || part < 0)
+    return fail(FSMC_ERR_ARG, "advance_prior_part needs nu, req_chain, req_count and a part index");
+  return advance_common(7, k, t, st, n, variant, order, tick_limit, mode, out, nullptr, nullptr, nu,
+                        req_chain, req_count, lanes, stream_, nullptr, j_lo, j_hi, part);
 }
 
 // nu[r] = L nu[r] in place, every row summed in the sampling kernel's order

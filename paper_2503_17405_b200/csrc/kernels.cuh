@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_advance_kernel(
   while (true) {
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
-    j = grp.bcast_ll(j, 0);
-    if (j >= p.st.m) break;
+    j = p.j_lo + grp.bcast_ll(j, 0);
+    if (j >= p.j_hi) break;
     Core c;
     core_load(c, p, j);
     c.ws = ws;
@@ -448,11 +448,11 @@ struct Launch {
     return persistent(fsm_window_kernel<F, G, E, TK, 0>, p, lc, s, sb, p.j_hi - p.j_lo);
   }
   static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
-    return persistent(fsm_advance_kernel<F, G, E>, p, lc, s);
+    return persistent(fsm_advance_kernel<F, G, E>, p, lc, s, 0, p.j_hi - p.j_lo);
   }
   // fsmc_advance_prior: evaluations inline, parked only at the prior transform
   static cudaError_t advance_prior(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
-    return persistent(fsm_advance_kernel<F, G, E, TK, true>, p, lc, s);
+    return persistent(fsm_advance_kernel<F, G, E, TK, true>, p, lc, s, 0, p.j_hi - p.j_lo);
   }
   static cudaError_t lockstep(Params p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;

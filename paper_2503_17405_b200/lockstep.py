@@ -355,7 +355,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     bundled_order: tuple | None = None, record_sample_ticks: bool = False,
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
                     lanes: int = 0, evaluator=None, draw_window: int = 0,
-                    prior_transform=None, draw_parts: int = 1, _timing: dict | None = None):
+                    prior_transform=None, draw_parts: int = 1, prior_parts: int = 1,
+                    _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
@@ -379,7 +380,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     "trmm": the same product as a triangular cuBLAS DTRMM (half the flops);
     "device": ``fsmc_prior_apply``, the sampling kernel's summation order
     (bit-identical to the default mode); or a callable ``f(nu[k, d])``
-    transforming the rows in place.
+    transforming the rows in place.  ``prior_parts`` (1..8) splits the chains
+    in parts whose rounds overlap on their own streams.
 
     ``draw_window`` (DRMH kernels): generate each chain's next ``draw_window``
     PRNG draws in a separate full-occupancy kernel and let the step kernel
@@ -422,7 +424,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         if target.struct().prior_kind != _lib.PRIOR_DENSE:
             prior_transform = None      # identity prior: nu = eps, nothing to batch
     if prior_transform is not None:
-        launch = _prior_launcher(target, batch, n, variant, ordv, out, lanes, prior_transform)
+        launch = _prior_launcher(target, batch, n, variant, ordv, out, lanes, prior_transform,
+                                 prior_parts)
     elif draw_window:
         # [m][window] plus a line of slack: the step kernel prefetches the
         # next proposal's draws, which for the last chain may lie past its window
@@ -536,39 +539,73 @@ def _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evalu
     return launch
 
 
-def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform):
+_SIDE_STREAMS: list = []      # reused across runs (prior_parts)
+
+
+def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, parts=1):
     """Rounds of fsmc_advance_prior + one batched nu = L eps over every
-    chain parked at INIT."""
+    chain parked at INIT.  parts > 1: the chains in contiguous parts, each
+    with its own rounds on its own stream (fsmc_advance_prior_part), so one
+    part's transform overlaps another part's advance kernel."""
     m, d = batch.m, target.dim
+    parts = max(1, min(int(parts), 8, m))
+    bounds = [(m * h // parts, m * (h + 1) // parts) for h in range(parts)]
     nu = torch.empty((m, d), dtype=torch.float64, device="cuda")
     req_chain = torch.empty(m, dtype=torch.int32, device="cuda")
-    req_count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    req_count = torch.zeros(parts, dtype=torch.int32, device="cuda")
     lib = _lib.lib()
     kern, tgt = batch.kernel, target.struct()
     if transform in ("gemm", "trmm"):
         from .dense import PriorTransform
-        transform = PriorTransform(target.device_arrays()["prior_t"], transform)
+        transform = [PriorTransform(target.device_arrays()["prior_t"], transform)
+                     for _ in range(parts)]
+        for h, t in enumerate(transform):    # scratch allocated up front, on this stream
+            t.tmp = torch.empty((bounds[h][1] - bounds[h][0], d), dtype=torch.float64, device="cuda")
     elif transform == "device":
         def transform(rows):
             _lib.check(lib.fsmc_prior_apply(ctypes.byref(tgt), rows.data_ptr(), rows.shape[0],
                                             _lib.stream_ptr()), "fsmc_prior_apply")
     elif not callable(transform):
         raise ValueError("prior_transform must be 'trmm', 'gemm', 'device' or a callable")
+    if not isinstance(transform, list):
+        transform = [transform] * parts
     stats = {"rounds": 0, "prior_transforms": 0}
+    main = torch.cuda.current_stream()
+    while len(_SIDE_STREAMS) < parts - 1:
+        _SIDE_STREAMS.append(torch.cuda.Stream())
+    streams = [main] + _SIDE_STREAMS[:parts - 1]
+
+    def advance(h, mode, tick_limit):
+        lo, hi = bounds[h]
+        _lib.check(lib.fsmc_advance_prior_part(
+            ctypes.byref(kern), ctypes.byref(tgt), ctypes.byref(batch.struct()), n, variant, ordv,
+            tick_limit, mode, ctypes.byref(out), nu[lo:].data_ptr(), req_chain[lo:].data_ptr(),
+            req_count[h:].data_ptr(), lanes, lo, hi, h, _lib.stream_ptr()),
+            "fsmc_advance_prior_part")
 
     def launch(mode, tick_limit):
-        while True:
-            _lib.check(lib.fsmc_advance_prior(ctypes.byref(kern), ctypes.byref(tgt),
-                                              ctypes.byref(batch.struct()), n, variant, ordv,
-                                              tick_limit, mode, ctypes.byref(out), nu.data_ptr(),
-                                              req_chain.data_ptr(), req_count.data_ptr(), lanes,
-                                              _lib.stream_ptr()), "fsmc_advance_prior")
-            k = int(req_count.item())
-            if k == 0:
-                return
-            stats["rounds"] += 1
-            stats["prior_transforms"] += k
-            transform(nu[:k])
+        for s in streams[1:]:
+            s.wait_stream(main)
+        active = list(range(parts))
+        for h in active:
+            with torch.cuda.stream(streams[h]):
+                advance(h, mode, tick_limit)
+        while active:
+            still = []
+            for h in active:
+                with torch.cuda.stream(streams[h]):
+                    k = int(req_count[h].item())
+                    if k == 0:
+                        continue
+                    stats["rounds"] += 1
+                    stats["prior_transforms"] += k
+                    lo = bounds[h][0]
+                    transform[h](nu[lo:lo + k])
+                    advance(h, mode, tick_limit)
+                    still.append(h)
+            active = still
+        for s in streams[1:]:
+            main.wait_stream(s)
 
     launch.stats = stats
     return launch
