@@ -133,6 +133,8 @@ enum { FSMC_E_NONE = 0, FSMC_E_BLOCK = 1, FSMC_E_ZERO_START = 2, FSMC_E_GRAD = 3
        FSMC_E_TARGET = 5 /* the plugin itself failed (TargetError, e.g. a kernel matrix not PD) */ };
 
 int32_t fsmc_abi_version(void);
+/* Kernels this library has launched so far (all entry points, all streams). */
+int64_t fsmc_launch_count(void);
 const char* fsmc_last_error(void);
 
 /* Slots a chain of this kernel needs (vectors of `dim` doubles, scalars). */

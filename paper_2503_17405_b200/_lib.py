@@ -87,6 +87,7 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     S = ctypes.c_int
     L.fsmc_abi_version.restype = ctypes.c_int32
+    L.fsmc_launch_count.restype = ctypes.c_int64
     L.fsmc_last_error.restype = ctypes.c_char_p
     L.fsmc_state_layout.restype = S
     L.fsmc_state_layout.argtypes = [ctypes.POINTER(Kernel), ctypes.c_int64] + \

@@ -70,6 +70,7 @@ static cudaError_t launch_drmh_draws(const Params& p, int num_sms, cudaStream_t 
   long long need = (p.j_hi - p.j_lo + nw - 1) / nw;
   const int per_sm = p.draw_blocks_per_sm > 0 ? p.draw_blocks_per_sm : 8;
   int blocks = (int)std::max<long long>(1, std::min<long long>(need, (long long)num_sms * per_sm));
+  count_launch();
   drmh_draws_kernel<<<blocks, threads, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -328,6 +328,8 @@ fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_st
 extern "C" {
 
 int32_t fsmc_abi_version(void) { return FSMC_ABI_VERSION; }
+
+int64_t fsmc_launch_count(void) { return fsmc::launch_counter().load(); }
 const char* fsmc_last_error(void) { return g_last_error.c_str(); }
 
 fsmc_status fsmc_state_layout(const fsmc_kernel* k, int64_t dim, int32_t* n_vec, int32_t* n_scal,
@@ -354,6 +356,7 @@ fsmc_status fsmc_prng_fill(uint64_t seed, uint64_t stream, uint64_t counter, int
   if (count < 0 || kind < 0 || kind > 2 || (!out && count)) return fail(FSMC_ERR_ARG, "bad prng_fill args");
   if (!count) return FSMC_OK;
   int blocks = (int)std::min<long long>((count + 255) / 256, 148LL * 16);
+  fsmc::count_launch();
   prng_fill_kernel<<<blocks, 256, 0, (cudaStream_t)stream_>>>(seed, stream, counter, count, kind, out);
   CUDA_TRY(cudaGetLastError());
   return FSMC_OK;
@@ -563,6 +566,7 @@ fsmc_status fsmc_prior_apply(const fsmc_target* t, double* nu, int64_t k, void* 
   if (sb > 48 * 1024)
     CUDA_TRY(cudaFuncSetAttribute((const void*)prior_apply_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+  fsmc::count_launch();
   prior_apply_kernel<<<(unsigned)k, 256, sb, (cudaStream_t)stream_>>>(t->prior_t, nu, (int)t->dim);
   CUDA_TRY(cudaGetLastError());
   return FSMC_OK;
@@ -741,6 +745,7 @@ fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, d
 #define X(GG, EE)                                                                           \
   if (ge.g == GG && ge.e == EE) {                                                           \
     CUDA_TRY(allow_smem(target_eval_kernel<GG, EE>, smem_bytes<GG, EE>(group_doubles(tt))));     \
+    fsmc::count_launch();                                                         \
     target_eval_kernel<GG, EE><<<blocks, kThreads, smem_bytes<GG, EE>(group_doubles(tt)), cs>>>(tt, X, m, lp, grad); \
     CUDA_TRY(cudaGetLastError());                                                         \
     return FSMC_OK;                                                                       \
@@ -756,6 +761,7 @@ fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, i
   if (!rows) return FSMC_OK;
   if (rows > 65535) return fail(FSMC_ERR_ARG, "at most 65535 rows per epilogue call");
   dim3 grid((unsigned)((N + kEpiCols - 1) / kEpiCols), (unsigned)rows);
+  fsmc::count_launch();
   logreg_epilogue_kernel<<<grid, 256, 0, (cudaStream_t)stream_>>>(Z, y, N, R, lp);
   CUDA_TRY(cudaGetLastError());
   return FSMC_OK;
@@ -768,6 +774,7 @@ fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int6
   cudaStream_t cs = (cudaStream_t)stream_;
   if (lag0 == 0) {
     long long tot = m * dim;
+    fsmc::count_launch();
     diag_mean_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, cs>>>(samples, n, m, dim, burn, chain_mean);
     CUDA_TRY(cudaGetLastError());
   }
@@ -776,6 +783,7 @@ fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int6
     CUDA_TRY(cudaMemsetAsync(acov, 0, sizeof(double) * kLagTile * dim, cs));
     long long tot = m * dim;
     size_t sm = dim <= 128 ? sizeof(double) * kLagTile * dim : 0;
+    fsmc::count_launch();
     diag_acov_kernel<<<(unsigned)((tot + 127) / 128), 128, sm, cs>>>(samples, n, m, dim, burn, lag0,
                                                                      chain_mean, acov, chain_var);
     CUDA_TRY(cudaGetLastError());

@@ -24,6 +24,7 @@
 #include <string>
 
 #include "../../include/fsmc.h"
+#include "launch_count.h"
 
 namespace {
 
@@ -211,6 +212,7 @@ fsmc_status fsmc_gp_lml(const double* theta, int64_t k, const double* d2, const 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
   if (e == cudaSuccess) {
     const int grid = (int)(k < work_slots ? k : work_slots);
+    fsmc::count_launch();
     gp_lml_kernel<<<grid, THREADS, sb, (cudaStream_t)stream_>>>(theta, (int)k, d2, y, (int)n, jitter,
                                                                  residual, work, lp);
     e = cudaGetLastError();

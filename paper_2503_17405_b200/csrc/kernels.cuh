@@ -13,6 +13,7 @@
 
 #include "configs.h"
 #include "fsm_device.cuh"
+#include "launch_count.h"
 
 namespace fsmc {
 
@@ -404,12 +405,14 @@ struct Launch {
     int blocks = (int)std::min<long long>(groups, 1 << 20);
     cudaError_t e = allow_smem(fsm_init_kernel<F, G, E>, smem(p));
     if (e != cudaSuccess) return e;
+    count_launch();
     fsm_init_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p, ps, off, x0, jit);
     return cudaGetLastError();
   }
   static cudaError_t init_finish(const Params& p, cudaStream_t s) {
     long long groups = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
     int blocks = (int)std::min<long long>(groups, 1 << 20);
+    count_launch();
     fsm_init_finish_kernel<F, G, E><<<blocks, kThreads, 0, s>>>(p);
     return cudaGetLastError();
   }
@@ -427,6 +430,7 @@ struct Launch {
     if (chains < 0) chains = p.st.m;
     long long need = (chains + (kThreads / G) - 1) / (kThreads / G);
     int blocks = (int)std::max<long long>(1, std::min<long long>(need, (long long)occ * lc.num_sms));
+    count_launch();
     kern<<<blocks, kThreads, sb, s>>>(p);
     return cudaGetLastError();
   }
@@ -469,6 +473,7 @@ struct Launch {
       p.wave_hi = std::min<long long>(p.st.m, lo + cap);
       int blocks = (int)((p.wave_hi - lo + per_block - 1) / per_block);
       void* args[] = {&p};
+      count_launch();
       e = cudaLaunchCooperativeKernel((const void*)lockstep_kernel<F, G, E, TK>, dim3(blocks),
                                       dim3(kThreads), args, smem(p), s);
       if (e != cudaSuccess) return e;

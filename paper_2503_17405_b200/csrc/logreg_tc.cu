@@ -30,6 +30,7 @@
 #include <string>
 
 #include "../../include/fsmc.h"
+#include "launch_count.h"
 
 namespace {
 
@@ -396,6 +397,7 @@ fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16
   if (!k) return FSMC_OK;
   cudaStream_t s = (cudaStream_t)stream_;
   const long long kpad = (k + BM - 1) / BM * BM;
+  fsmc::count_launch(2);   // this and logreg_tc_kernel
   to_bf16_kernel<<<(unsigned)((kpad * DF + 255) / 256), 256, 0, s>>>(theta, k, kpad, (__nv_bfloat16*)theta_bf16);
   CUtensorMap mt, mx, mxt;
   if (!make_map(&mt, theta_bf16, kpad, DF, BM) || !make_map(&mx, x_bf16, n_obs, DF, BN) ||
