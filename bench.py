@@ -45,7 +45,7 @@ CONFIGS = {
                         "scale=0.1, bundled", family="drmh", m=65536, n=1000, d=10,
                variant="bundled", m_cpu=256, draw_window=3300, draw_parts=4),
     "c1": dict(workload="C1: elliptical slice FSM, conjugate Gaussian-likelihood d=100, amortized",
-               family="ess", m=128, n=1000, d=100, variant="amortized", m_cpu=32),
+               family="ess", m=128, n=1000, d=100, variant="amortized", m_cpu=32, lanes=128),
     "c3": dict(workload="C3: NUTS FSM, equicorrelated Gaussian d=100 rho=0.99, eps=0.05, depth 10",
                family="nuts", m=16384, n=1000, d=100, variant="bundled", m_cpu=16),
     "c4": dict(workload="C4: elliptical slice FSM, GP-classification latent d=1024 (f-space)",
@@ -203,6 +203,8 @@ def main():
         cfg["n"] = args.n
     if args.draw_window >= 0:
         cfg["draw_window"] = args.draw_window
+    if not args.lanes and cfg.get("lanes"):
+        args.lanes = cfg["lanes"]     # e.g. C1: 128 chains, a whole block per chain
     if args.draw_parts:
         cfg["draw_parts"] = args.draw_parts
     if args.prior_parts:
