@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
     for (int c0 = 0; c0 < W; c0 += kDrawChunk) {
       const int c1 = min(W, c0 + kDrawChunk);
       int nt = 0;
+#pragma unroll 4
       for (int k0 = c0; k0 < c1; k0 += 32) {
         // branch-free: every lane evaluates the central branch (uniform and
         // tail lanes discard it), so the warp never splits three ways
