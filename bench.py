@@ -43,7 +43,7 @@ FP64_FLOPS_PER_PROPOSAL = 976.0
 CONFIGS = {
     "c2": dict(workload="C2: DRMH FSM, correlated MoG d=10 (rho=0.9, modes -3/0/3), M=100, "
                         "scale=0.1, bundled", family="drmh", m=65536, n=1000, d=10,
-               variant="bundled", m_cpu=256, draw_window=3300, draw_parts=4),
+               variant="bundled", m_cpu=256, draw_window=4070, draw_parts=4),
     "c1": dict(workload="C1: elliptical slice FSM, conjugate Gaussian-likelihood d=100, amortized",
                family="ess", m=128, n=1000, d=100, variant="amortized", m_cpu=32, lanes=128),
     "c3": dict(workload="C3: NUTS FSM, equicorrelated Gaussian d=100 rho=0.99, eps=0.05, depth 10",
@@ -382,7 +382,7 @@ def main():
     if draw_bytes:
         roof["frac_without_draws"] = (st_bytes + out_bytes) / (kms / 1e3) / 1e9 / peaks["hbm_gbs"]
         tp = os.path.join(ROOT, "profiles", "r02_c2_traffic.json")
-        if os.path.exists(tp) and cfg.get("draw_window") == 3300:
+        if os.path.exists(tp) and cfg.get("draw_window") in (3300, 4070):
             # ncu DRAM bytes of one generator + window launch pair (draws + 4%:
             # state and samples), scaled to this run by its draw bytes
             t = json.load(open(tp))
