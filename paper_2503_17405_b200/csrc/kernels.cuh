@@ -50,6 +50,10 @@ inline cudaError_t allow_smem(K* kern, size_t bytes) {
 #endif
 template <int G>
 __host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : (G == 32 ? FSMC_WARP_MIN_BLOCKS : (G == 128 ? 4 : 1)); }
+// block-per-chain NUTS (G = 128, C5's advance kernel) keeps its registers: 4
+// resident blocks would spill its twelve-vector state
+template <template <int, int> class F, int G, int E>
+__host__ __device__ constexpr int min_blocks_for() { return (G == 128 && F<G, E>::GRAD) ? 1 : min_blocks<G>(); }
 
 struct LaunchCtx {
   int num_sms;
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) fsm_init_finish_kernel(Params p) {
 // with its state in registers.  No barrier anywhere: chains in different
 // states simply execute different blocks.
 template <template <int, int> class F, int G, int E, int TK, int VAR = 0>
-__global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_run_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
   double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_profile_kernel(
 // Batched-evaluation mode: every chain runs to its next log-density request
 // and parks the point in the compact request list (see fsmc_advance).
 template <template <int, int> class F, int G, int E, int TK = 0, bool INLINE = false>
-__global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_advance_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_advance_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
   double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
