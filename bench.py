@@ -375,10 +375,32 @@ def main():
             "kernel": ("drmh_draws_kernel + fsm_window_kernel<DrmhW,1,10,MOG>" if win else
                        "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel"),
             "kernel_ms": kms, "algorithmic_bytes": traffic_bytes,
-            "note": "HBM carries samples, ledger rows, chain state and (windowed) the pre-drawn "
-                    "normals/uniforms, 16 B per draw (written by drmh_draws_kernel, read by "
-                    "fsm_window_kernel: a design choice, see frac_without_draws); the run is "
-                    "fp64/integer issue-bound: see 'compute' and profiles/"}
+            "note": ("HBM carries samples, ledger rows, chain state and (windowed) the pre-drawn "
+                     "normals/uniforms, 16 B per draw (written by drmh_draws_kernel, read by "
+                     "fsm_window_kernel: a design choice, see frac_without_draws); the run is "
+                     "fp64/integer issue-bound: see 'compute' and profiles/") if win else
+                    ("HBM carries samples, ledger rows and chain state loaded/stored once per "
+                     "launch; the per-chain FSM state stays in registers/shared memory for the "
+                     "whole run, so the kernel is fp64-issue/latency-bound, not HBM-bound: "
+                     "'state_model' gives the SURVEY.md 8(d) per-unit figure")}
+    # SURVEY.md 8(d) per-unit bytes: the traffic an SoA-state-in-HBM step kernel would
+    # move per unit (chain-tick, or INTEGRATE chain-tick for NUTS).  This kernel keeps
+    # that state on chip, so this is an equivalent bandwidth, not DRAM traffic.
+    n_inner = int(ledger.iter_counts.sum().item()) if hasattr(ledger.iter_counts, "sum") else 0
+    if cfg["family"] == "ess":
+        units, per_unit, uname = n_inner + 2 * n * m, 2 * d * 8 + 96 + 3 * d * 8 * n * m / \
+            max(1, n_inner + 2 * n * m), "chain-tick (INIT, SHRINK, DONE)"
+    elif cfg["family"] == "nuts":
+        units, per_unit, uname = n_inner, 9.3 * d * 8 + 100, "INTEGRATE chain-tick (leapfrog)"
+    else:
+        units, per_unit, uname = n_inner, 2 * d * 8 + 96 + 2 * d * 8 * n * m / max(1, n_inner), \
+            "PROPOSE chain-tick"
+    if units:
+        sm_ach = units * per_unit / (kms / 1e3) / 1e9
+        roof["state_model"] = {"unit": uname, "units": units, "bytes_per_unit": per_unit,
+                               "achieved": sm_ach, "peak": peaks["hbm_gbs"], "unit_bw": "GB/s",
+                               "frac": sm_ach / peaks["hbm_gbs"],
+                               "source": "SURVEY.md 8(d) per-unit bytes x units / kernel time"}
     if draw_bytes:
         roof["frac_without_draws"] = (st_bytes + out_bytes) / (kms / 1e3) / 1e9 / peaks["hbm_gbs"]
         tp = os.path.join(ROOT, "profiles", "r02_c2_traffic.json")
