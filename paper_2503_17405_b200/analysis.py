@@ -118,9 +118,13 @@ def diag_moments(chains, burn: int = 0) -> DiagMoments:
 class _Acov:
     """Mean (over chains) autocovariance of one dimension set: lag tiles on
     demand, switching to one FFT over every lag once the truncation point is
-    beyond a few tiles."""
+    beyond a few tiles and the tiles left to reach n cost more than the FFT."""
 
     TILE_LIMIT = 3
+    # one all-lags transform costs about as much as this many lag-tile passes
+    # (tools/acov_probe.py: 45 ms against 1.7 ms per tile at C3's size), so
+    # short chains (C4: n = 180 rows, 6 tiles in all) stay on the tiles
+    FFT_TILE_EQUIV = 16
 
     def __init__(self, mom: DiagMoments):
         self.mom = mom
@@ -131,7 +135,8 @@ class _Acov:
         if self.full is not None:
             return float(self.full[t, k]) if t < self.full.shape[0] else 0.0
         tile = t // LAG_TILE
-        if tile >= self.TILE_LIMIT and self.mom.acov_all is not None:
+        if (tile >= self.TILE_LIMIT and self.mom.acov_all is not None
+                and -(-self.mom.n // LAG_TILE) - len(self.tiles) > self.FFT_TILE_EQUIV):
             self.full = self.mom.acov_all() / self.mom.m
             return self(t, k)
         while len(self.tiles) <= tile:
@@ -245,13 +250,17 @@ def _acf_for_geyer(mom: DiagMoments) -> np.ndarray:
         acf = _acf_tiles(mom, tiles)
     if acf is not None:
         return acf
-    if mom.acov_all is not None:
+    if _fft_pays(mom, len(tiles)):
         return mom.acov_all()[:n] / mom.m
-    while True:
+    while len(tiles) * LAG_TILE < n:
         tiles.append(mom.acov_tile(len(tiles)) / mom.m)
-        acf = np.vstack(tiles)[:n]
-        if acf.shape[0] >= n:
-            return acf
+    return np.vstack(tiles)[:n]
+
+
+def _fft_pays(mom: DiagMoments, tiles_done: int) -> bool:
+    """The all-lags transform beats the lag tiles still needed to reach n."""
+    return (mom.acov_all is not None
+            and -(-mom.n // LAG_TILE) - tiles_done > _Acov.FFT_TILE_EQUIV)
 
 
 def _acf_tiles(mom: DiagMoments, tiles: list):
@@ -272,7 +281,7 @@ def _acf_tiles(mom: DiagMoments, tiles: list):
             return acf
         # a dimension still correlated at 0.5 at the last lag fetched will need
         # far more tiles: go to the all-lags transform at once
-        if mom.acov_all is not None and bool((rho[-1][~done] > 0.5).any()):
+        if _fft_pays(mom, len(tiles)) and bool((rho[-1][~done] > 0.5).any()):
             return None
     return None
 

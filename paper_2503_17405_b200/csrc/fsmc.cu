@@ -121,21 +121,25 @@ constexpr int kLagTile = 32;
 __global__ void __launch_bounds__(128) diag_acov_kernel(const double* __restrict__ S, long long n, long long m,
                                                         long long d, long long burn, long long lag0,
                                                         const double* __restrict__ mean, double* acov,
-                                                        double* chain_var) {
+                                                        double* chain_var, long long cpt) {
   extern __shared__ double red[];   // [32][d] when d <= 128
   const bool smem_red = d <= 128;
   if (smem_red) {
     for (int i = threadIdx.x; i < kLagTile * d; i += blockDim.x) red[i] = 0.0;
     __syncthreads();
   }
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool live = idx < m * d;
-  const long long k = live ? idx % d : 0;
+  // cpt > 1 (wide targets, lag tiles past the first): a thread sums the lags
+  // of chains jg, jg + mg, ... of its dimension k before its global atomics
+  const long long mg = (m + cpt - 1) / cpt;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool live = g < mg * d;
+  const long long k = live ? g % d : 0;
   const long long N = n - burn;
   double acc[kLagTile];
 #pragma unroll
   for (int t = 0; t < kLagTile; t++) acc[t] = 0.0;
-  if (live) {
+  for (long long jj = live ? g / d : m; jj < m; jj += mg) {
+    const long long idx = jj * d + k;
     const double mu = mean[idx];
     const size_t stride = (size_t)m * d;
     const double* col = S + (size_t)burn * stride + idx;
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(128) diag_acov_kernel(const double* __restrict
         ring[q] = b_at(i + kLagTile);   // slot q now holds b_{i+32}
       }
     }
-    if (lag0 == 0 && chain_var) chain_var[idx] = acc[0] / (double)N;
+    if (lag0 == 0 && chain_var) chain_var[idx] = acc[0] / (double)N;   // cpt == 1 here
   }
   if (smem_red) {
     if (live) {
@@ -783,9 +787,13 @@ fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int6
     CUDA_TRY(cudaMemsetAsync(acov, 0, sizeof(double) * kLagTile * dim, cs));
     long long tot = m * dim;
     size_t sm = dim <= 128 ? sizeof(double) * kLagTile * dim : 0;
+    // wide targets reduce in global atomics: past the first tile (no per-chain
+    // variance), each thread folds 8 chains first
+    const long long cpt = (dim > 128 && lag0 > 0) ? 8 : 1;
+    tot = ((m + cpt - 1) / cpt) * dim;
     fsmc::count_launch();
     diag_acov_kernel<<<(unsigned)((tot + 127) / 128), 128, sm, cs>>>(samples, n, m, dim, burn, lag0,
-                                                                     chain_mean, acov, chain_var);
+                                                                     chain_mean, acov, chain_var, cpt);
     CUDA_TRY(cudaGetLastError());
   }
   return FSMC_OK;
