@@ -219,20 +219,29 @@ def _geyer_all(acf: np.ndarray, mom: DiagMoments) -> tuple[np.ndarray, np.ndarra
     odd_kept = (js < J[None, :]) | ((js == J[None, :]) & (P >= 0.0))  # rho[2j+1] stored?
     Pm = rho[0::2][:npairs] + np.where(odd_kept | (js == 0), rho[1::2][:npairs], 0.0)
     # initial monotone sequence over pairs 1..J: running minimum of pair sums
-    run = Pm.copy()
-    modified = np.zeros_like(run, dtype=bool)
-    for j in range(1, int(J.max()) + 1 if d else 1):
-        act = j <= J
-        mod = act & (run[j] > run[j - 1])
-        run[j] = np.where(mod, run[j - 1], run[j])
-        modified[j] = mod
+    # (pair j takes the minimum so far when it exceeds it: a cumulative minimum;
+    # min is exact, so the values equal the reference loop's)
+    cm = np.minimum.accumulate(Pm, axis=0)
+    act = (js >= 1) & (js <= J[None, :])
+    modified = np.zeros_like(Pm, dtype=bool)
+    modified[1:] = act[1:] & (Pm[1:] > cm[:-1])
+    run = np.where(act, cm, Pm)
     ev = np.where(modified, run / 2.0, rho[0::2][:npairs])
     od = np.where(modified, run / 2.0, np.where(odd_kept | (js == 0), rho[1::2][:npairs], 0.0))
     # tau = -1 + 2 sum_{i < 2J+1} rho_i: numpy's pairwise sum of each
     # dimension's contiguous rho[:max_t] (analysis.py:378)
     seq = np.empty((d, 2 * npairs))
     seq[:, 0::2], seq[:, 1::2] = ev.T, od.T
-    S = np.array([seq[k, :2 * J[k] + 1].sum() for k in range(d)])
+    # dimensions with the same length sum together: a reduction along the
+    # contiguous last axis runs the same pairwise sum per row
+    lengths = np.unique(J)
+    if 4 * lengths.size <= d:
+        S = np.empty(d)
+        for L in lengths:
+            ks = np.nonzero(J == L)[0]
+            S[ks] = np.ascontiguousarray(seq[ks, :2 * L + 1]).sum(axis=1)
+    else:
+        S = np.array([seq[k, :2 * J[k] + 1].sum() for k in range(d)])
     tau = -1.0 + 2.0 * S
     bad = (tau <= 0) | ~np.isfinite(tau)
     tau = np.where(bad, 1.0 / total, tau)
