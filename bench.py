@@ -52,11 +52,18 @@ CONFIGS = {
                family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4,
                prior_transform="trmm", prior_parts=3),
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
-                        "depth 10; batched TF32 gradient evaluation across chains",
+                        "depth 10; fp64 chain state, log density and gradient by the fused "
+                        "tcgen05 kernel across chains (bf16 operands, fp32 accumulation)",
                family="nuts", m=131072, n=32, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
                batched="bf16-tc"),
 }
 
+
+# arithmetic of the line: fp64 everywhere unless a reduced-precision batched
+# evaluator computes the log density and gradient
+EVAL_DTYPE = {"bf16-tc": "f64 state / bf16 evaluator (fp32 accumulate)",
+              "tf32-tc": "f64 state / tf32 evaluator (fp32 accumulate)",
+              "tf32": "f64 state / tf32 evaluator (cuBLAS)"}
 
 _LOGREG = {}
 
@@ -451,7 +458,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic",
+                "dtype": EVAL_DTYPE.get(cfg.get("batched"), "f64"), "data": "synthetic",
                 "config": {"workload": cfg["workload"], "chains_per_gpu": m, "chains_total": m * world,
                            "n": n, "d": d, "variant": cfg["variant"],
                            "parallelism": f"chains sharded over {world} GPU(s), no data-path "

@@ -22,7 +22,8 @@
 extern "C" {
 #endif
 
-#define FSMC_ABI_VERSION 3
+#define FSMC_ABI_VERSION 4
+#define FSMC_WORK_WORDS 256 /* uint32 words of fsmc_state.work */
 #define FSMC_NINT 32        /* int64 slots per chain in fsmc_state.ints */
 #define FSMC_MAX_MODES 8    /* mixture components in FSMC_T_MOG */
 
@@ -110,6 +111,11 @@ typedef struct fsmc_state {
   int64_t* ints;                /* [m][FSMC_NINT] */
   uint64_t seed;
   unsigned long long* err_key;  /* [1]; (tick << 24) | chain of the first failure, ~0 = none */
+  uint32_t* work;               /* [FSMC_WORK_WORDS] device words owned by this state block: the
+                                   chain queues and barrier words of the launches that run it
+                                   (contents need not be initialised).  Two state blocks never
+                                   share launch bookkeeping, so runs of different blocks may
+                                   proceed concurrently on different streams and devices. */
 } fsmc_state;
 
 /* Per-sample observables of the CostLedger (lockstep.py:209-228). */

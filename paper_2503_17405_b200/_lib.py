@@ -15,7 +15,8 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FSMC_LIB", os.path.join(HERE, "libfsmc.so"))
 
-ABI_VERSION = 3    # fsmc.h FSMC_ABI_VERSION
+ABI_VERSION = 4    # fsmc.h FSMC_ABI_VERSION
+WORK_WORDS = 256   # fsmc.h FSMC_WORK_WORDS
 FSMC_NINT = 32
 MAX_MODES = 8
 
@@ -63,7 +64,7 @@ class Target(ctypes.Structure):
 class State(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int64), ("dim", ctypes.c_int64), ("n_vec", ctypes.c_int32),
                 ("n_scal", ctypes.c_int32), ("vec", _P), ("scal", _P), ("ints", _P),
-                ("seed", ctypes.c_uint64), ("err_key", _P)]
+                ("seed", ctypes.c_uint64), ("err_key", _P), ("work", _P)]
 
 
 class Outputs(ctypes.Structure):

@@ -213,9 +213,10 @@ def _geyer_all(acf: np.ndarray, mom: DiagMoments) -> tuple[np.ndarray, np.ndarra
     # P_j < 0, or the last j with 2j - 1 < n - 2
     j_lim = max(0, (n - 2) // 2)                       # largest j with 2j - 1 < n - 2
     js = np.arange(npairs)[:, None]
-    neg = (P < 0.0) & (js >= 1) & (js <= j_lim)
+    # the reference loop runs while a pair sum is >= 0: a NaN pair stops it too
+    neg = ~(P >= 0.0) & (js >= 1) & (js <= j_lim)
     first_neg = np.where(neg.any(axis=0), neg.argmax(axis=0), j_lim)
-    J = np.where(anticorrelated, 0, first_neg)                     # [d]
+    J = np.where(~(P[0] >= 0.0), 0, first_neg)                     # [d]
     odd_kept = (js < J[None, :]) | ((js == J[None, :]) & (P >= 0.0))  # rho[2j+1] stored?
     Pm = rho[0::2][:npairs] + np.where(odd_kept | (js == 0), rho[1::2][:npairs], 0.0)
     # initial monotone sequence over pairs 1..J: running minimum of pair sums

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "kernels.cuh"
@@ -34,24 +35,37 @@ fsmc_status fail(fsmc_status s, const std::string& msg) {
       return fail(FSMC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// SM count of the current device (cached per device: a process may drive several)
+constexpr int kMaxDevices = 64;
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
+  static int sms[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return sms[dev];
 }
 
-// per-device scratch: chain queue, barrier words
-struct Scratch {
-  unsigned* words = nullptr;  // [0] queue, [1] bar_count, [2] bar_gen, [3..4] active flags
-};
-Scratch& scratch() {
-  static Scratch s;
-  if (!s.words) cudaMalloc(&s.words, 256 * sizeof(unsigned));
-  return s;
+// Side streams of the overlapped windowed run, created once per device.  The
+// launch bookkeeping (chain queues, barrier words) lives in each state
+// block's own fsmc_state.work, so nothing else is shared between calls.
+constexpr int kMaxParts = 8;
+std::mutex g_side_mu;
+cudaError_t side_streams(cudaStream_t (&out)[kMaxParts]) {
+  static cudaStream_t side[kMaxDevices][kMaxParts] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  for (int h = 1; h < kMaxParts; h++) {
+    if (!side[dev][h]) {
+      e = cudaStreamCreateWithFlags(&side[dev][h], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    out[h] = side[dev][h];
+  }
+  return cudaSuccess;
 }
 }  // namespace
 
@@ -282,7 +296,6 @@ int n_states(const fsmc_kernel* k) {
 LaunchCtx launch_ctx() {
   LaunchCtx lc;
   lc.num_sms = num_sms();
-  lc.words = scratch().words;
   return lc;
 }
 
@@ -302,6 +315,7 @@ fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_st
   if (k->family < FSMC_DRMH || k->family > FSMC_SLICE) return fail(FSMC_ERR_ARG, "unknown kernel family");
   if (t->dim < 1) return fail(FSMC_ERR_ARG, "dim must be >= 1");
   if (st->dim != t->dim) return fail(FSMC_ERR_ARG, "state dim does not match target dim");
+  if (!st->work || !st->err_key) return fail(FSMC_ERR_ARG, "state needs err_key[1] and work[FSMC_WORK_WORDS]");
   if (st->m < 1 || st->m >= (1LL << 24)) return fail(FSMC_ERR_ARG, "m must be in [1, 2^24) per state block");
   if (k->family == FSMC_DRMH && (k->max_tries < 1 || !(k->proposal_scale > 0)))
     return fail(FSMC_ERR_ARG, "invalid drmh parameters");
@@ -437,7 +451,7 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
     if (p.order[i] != (i == 0 ? K : i)) p.default_order = 0;
   }
   cudaStream_t cs = (cudaStream_t)stream_;
-  p.next_chain = scratch().words;
+  p.next_chain = st->work;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
   CUDA_TRY(dispatch_family(1, ge, p, cs));
   return FSMC_OK;
@@ -487,7 +501,7 @@ static fsmc_status advance_common(int op, const fsmc_kernel* k, const fsmc_targe
   }
   p.j_lo = j_lo;
   p.j_hi = j_hi;
-  p.next_chain = part < 0 ? scratch().words : scratch().words + 128 + 16 * part;
+  p.next_chain = part < 0 ? st->work : st->work + 128 + 16 * part;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
   CUDA_TRY(cudaMemsetAsync(req_count, 0, sizeof(int32_t), cs));
   CUDA_TRY(dispatch_family(op, ge, p, cs));
@@ -615,22 +629,19 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
   }
   p.draws = draws;
   p.window = window;
-  constexpr int kMaxParts = 8;
   if (parts < 1 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 1..8");
   if (st->m < parts) parts = 1;
   cudaStream_t cs = (cudaStream_t)stream_;
-  unsigned* w = scratch().words;
+  unsigned* w = st->work;
   // parts > 1: the chains in contiguous parts, each alternating its draw
   // generation and window kernels on its own stream, so one part's kernels
   // fill the SMs another part's kernel tail and launch gaps leave idle
-  static cudaStream_t side[kMaxParts] = {};
-  static cudaEvent_t ev_fork = nullptr, ev_join[kMaxParts] = {};
-  if (parts > 1 && !side[1]) {
+  cudaStream_t side[kMaxParts] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxParts] = {};
+  if (parts > 1) {
+    CUDA_TRY(side_streams(side));
     CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    for (int h = 1; h < kMaxParts; h++) {
-      CUDA_TRY(cudaStreamCreateWithFlags(&side[h], cudaStreamNonBlocking));
-      CUDA_TRY(cudaEventCreateWithFlags(&ev_join[h], cudaEventDisableTiming));
-    }
+    for (int h = 1; h < parts; h++) CUDA_TRY(cudaEventCreateWithFlags(&ev_join[h], cudaEventDisableTiming));
   }
   static int draw_bps = -1;   // draws-kernel blocks per SM (FSMC_DRAW_BLOCKS_PER_SM; 0 = fill)
   if (draw_bps < 0) {
@@ -680,7 +691,9 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
     for (int h = 1; h < parts; h++) {
       CUDA_TRY(cudaEventRecord(ev_join[h], sh[h]));
       CUDA_TRY(cudaStreamWaitEvent(cs, ev_join[h], 0));
+      CUDA_TRY(cudaEventDestroy(ev_join[h]));   // released once the wait completes
     }
+    CUDA_TRY(cudaEventDestroy(ev_fork));
   }
   return FSMC_OK;
 }
@@ -705,7 +718,7 @@ fsmc_status fsmc_profile_blocks(const fsmc_kernel* k, const fsmc_target* t, fsmc
   p.mode = 1;
   p.prof = cycles;
   cudaStream_t cs = (cudaStream_t)stream_;
-  p.next_chain = scratch().words;
+  p.next_chain = st->work;
   CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
   CUDA_TRY(dispatch_family(4, ge, p, cs));
   return FSMC_OK;
@@ -725,7 +738,7 @@ fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
   if (out) p.out = *out;
   p.n = n;
   cudaStream_t cs = (cudaStream_t)stream_;
-  unsigned* w = scratch().words;
+  unsigned* w = st->work;
   p.bar_count = w + 1;
   p.bar_gen = w + 2;
   p.active_flags = w + 3;

@@ -57,7 +57,6 @@ __host__ __device__ constexpr int min_blocks_for() { return (G == 128 && F<G, E>
 
 struct LaunchCtx {
   int num_sms;
-  unsigned* words;  // [0] chain queue, [1] barrier count, [2] barrier generation, [3..4] flags
 };
 
 // ---------------------------------------------------------------- init

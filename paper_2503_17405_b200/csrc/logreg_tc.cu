@@ -405,10 +405,14 @@ fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16
     g_err = "cuTensorMapEncodeTiled failed (alignment: n_obs must be a multiple of 8)";
     return FSMC_ERR_ARG;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(logreg_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr = true;
+  // the shared-memory opt-in is a per-device function attribute
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
+    cudaError_t ea = cudaFuncSetAttribute(logreg_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (ea != cudaSuccess) { g_err = cudaGetErrorString(ea); return FSMC_ERR_CUDA; }
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   logreg_tc_kernel<<<(unsigned)(kpad / BM), NTHREADS, SMEM_BYTES, s>>>(mt, mx, mxt, xty, theta, k, n_obs, lp,
                                                                       grad);

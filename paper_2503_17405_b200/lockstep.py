@@ -149,7 +149,8 @@ class ChainBatch:
 
     vec [m, n_vec, d] float64, scal [m, n_scal] float64, ints [m, 32] int64
     (counter, stream, state, tick, count, error record, block counts,
-    family-private integers), err_key [1].
+    family-private integers), err_key [1], work [256] int32 (the launch
+    bookkeeping of runs on this batch: chain queues, barrier words).
     """
 
     def __init__(self, bundle, target, m: int, seed: int, parent_stream: int = 0,
@@ -168,6 +169,7 @@ class ChainBatch:
         self.scal = torch.zeros((self.m, self.n_scal), dtype=torch.float64, device="cuda")
         self.ints = torch.zeros((self.m, _lib.FSMC_NINT), dtype=torch.int64, device="cuda")
         self.err_key = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        self.work = torch.zeros(_lib.WORK_WORDS, dtype=torch.int32, device="cuda")
         self.active_mask = [True] * self.m
         self._ran = False
 
@@ -182,6 +184,7 @@ class ChainBatch:
         s.ints = self.ints[lo].data_ptr()
         s.seed = self.seed & ((1 << 64) - 1)
         s.err_key = self.err_key.data_ptr()
+        s.work = self.work.data_ptr()
         return s
 
     # reference-shaped views (host copies)
@@ -539,7 +542,7 @@ def _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evalu
     return launch
 
 
-_SIDE_STREAMS: list = []      # reused across runs (prior_parts)
+_SIDE_STREAMS: dict = {}      # per device, reused across runs (prior_parts)
 
 
 def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, parts=1):
@@ -571,9 +574,10 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
         transform = [transform] * parts
     stats = {"rounds": 0, "prior_transforms": 0}
     main = torch.cuda.current_stream()
-    while len(_SIDE_STREAMS) < parts - 1:
-        _SIDE_STREAMS.append(torch.cuda.Stream())
-    streams = [main] + _SIDE_STREAMS[:parts - 1]
+    side = _SIDE_STREAMS.setdefault(main.device, [])
+    while len(side) < parts - 1:
+        side.append(torch.cuda.Stream(device=main.device))
+    streams = [main] + side[:parts - 1]
 
     def advance(h, mode, tick_limit):
         lo, hi = bounds[h]

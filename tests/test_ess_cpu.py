@@ -57,3 +57,24 @@ def test_ess_matches_reference_formula_on_draws(phi):
         got = A.ess_from_moments(mom).per_dimension
         ref = [ess_numpy(x[:, :, k].T) for k in range(d)]
     np.testing.assert_allclose(got, ref, rtol=1e-10)
+
+
+def test_vectorized_geyer_stops_at_nan_pair_like_the_reference_loop():
+    """The reference's truncation loop runs `while ... and pair_sum >= 0`
+    (analysis.py:353-374), so a NaN pair sum ends it exactly as a negative one
+    does; the vectorized form must agree (including a NaN in pair 0)."""
+    rng = np.random.default_rng(5)
+    warnings.simplefilter("ignore")
+    for case in range(200):
+        n, m, d = int(rng.integers(20, 200)), int(rng.integers(2, 5)), int(rng.integers(1, 5))
+        phi = rng.uniform(0.3, 0.99, size=d)
+        acf = (phi[None, :] ** np.arange(n)[:, None]) * rng.uniform(0.5, 2, size=d)
+        for k in range(d):
+            at = int(rng.integers(1, min(n, 40)))
+            acf[at, k] = np.nan
+        mom = _moments(acf * m, n, m, rng.uniform(0, 0.5, size=d), np.ones(d))
+        ac = A._Acov(mom)
+        ref = [A._ess_dim(ac, mom, k) for k in range(d)]
+        ess, bad, _ = A._geyer_all(A._acf_for_geyer(mom), mom)
+        got = [A.ess_from_moments(mom).per_dimension[k] for k in range(d)]
+        assert got == [e for e, _ in ref], case

@@ -31,7 +31,30 @@ def test_library_exports_every_declared_entry_point():
     for s in syms:
         assert hasattr(lib, s), s
     lib.fsmc_abi_version.restype = ctypes.c_int32
-    assert lib.fsmc_abi_version() == 3   # fsmc.h FSMC_ABI_VERSION
+    assert lib.fsmc_abi_version() == 4   # fsmc.h FSMC_ABI_VERSION
+
+
+def test_state_without_work_words_is_rejected_before_any_launch():
+    """Launch bookkeeping (chain queues, barrier words) lives in each state
+    block's own work[] words, so concurrent runs on different batches never
+    share it; a state without them is an argument error (no CUDA call made)."""
+    if not os.path.exists(LIB):
+        pytest.skip("libfsmc.so not built")
+    from paper_2503_17405_b200 import _lib as L
+    lib = ctypes.CDLL(LIB)
+    lib.fsmc_last_error.restype = ctypes.c_char_p
+    k = L.Kernel()
+    k.family, k.max_tries, k.proposal_scale = L.DRMH, 10, 0.1
+    t = L.Target()
+    t.kind, t.dim = 8, 2   # FSMC_T_FLAT
+    st = L.State()
+    st.m, st.dim, st.n_vec, st.n_scal = 4, 2, 2, 3
+    st.vec = st.scal = st.ints = st.err_key = 16   # never dereferenced: rejected first
+    st.work = None
+    out = L.Outputs()
+    rc = lib.fsmc_run(ctypes.byref(k), ctypes.byref(t), ctypes.byref(st), ctypes.c_int64(10), 0,
+                      None, ctypes.c_int64(1 << 40), 0, ctypes.byref(out), 0, None)
+    assert rc == 1 and b"work" in lib.fsmc_last_error()
 
 
 def test_library_is_sm100a():
