@@ -39,6 +39,8 @@ METRIC = "samples/sec & ESS/sec at m chains (1/2/4/8 B200); speed-up vs lock-ste
 # executed fp64 flops per DRMH proposal on the MoG d=10 target (ncu SASS op
 # counts, DFMA counted twice: generator 65.1 per draw x 11 + step kernel 260)
 FP64_FLOPS_PER_PROPOSAL = 976.0
+# ncu instruction counts of the C2 kernel pair (tools/gpujobs/r04_*.sh)
+ISSUE_PROFILE = "r04_c2_issue.json"
 
 CONFIGS = {
     "c2": dict(workload="C2: DRMH FSM, correlated MoG d=10 (rho=0.9, modes -3/0/3), M=100, "
@@ -334,34 +336,62 @@ def main():
         lock_value = world * m * n_lock / t_lock
         lock = {"value": lock_value, "unit": "samples/s", "ms_per_step": 1e3 * t_lock,
                 "speedup": value / lock_value, "n": n_lock, **lock_extra}
-        if cfg.get("prior_transform"):
-            lock["note"] = ("lock-step kernel forms nu = L eps per chain (no batched prior "
-                            "transform); FSM with the same per-chain transform: see --prior none")
+        lock.update(lockstep_accounting(args, cfg, fm, bundle, target, m, n_lock, off, ledger,
+                                        t_lock, value, lock_value, barrier, max_over_ranks, world,
+                                        evaluator))
 
-    # end-to-end through the public API: host x0 (pinned) -> device, run, ESS -> host
+    # end-to-end through the public API as a drop-in caller gets it: the start
+    # point from (pinned) host memory, init_batch, run_fsm_batched with the
+    # reference's output types -- samples [n, m, d] float64 and the ledger's
+    # int64 count matrices as host numpy arrays (output="numpy")
     x0_host = torch.zeros(d, dtype=torch.float64).pin_memory()
-    e2e_s = []
+
+    def e2e_run(s, output):
+        x0 = x0_host.to(dev, non_blocking=True)
+        batch = fm.init_batch(bundle, target, m, 500 + s, x0=x0, chain_offset=off)
+        return fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
+                                  output=output, surplus=False, lanes=args.lanes,
+                                  evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
+                                  prior_transform=cfg.get("prior_transform"),
+                                  draw_parts=cfg.get("draw_parts", 1),
+                                  prior_parts=cfg.get("prior_parts", 1))
+
+    e2e_s, led_h = [], None
+    for s in range(3):           # the first call also pins the host buffers (cached after)
+        smp = led_h = None
+        barrier()
+        t0 = time.perf_counter()
+        smp, led_h = e2e_run(s, "numpy")
+        barrier()
+        e2e_s.append(time.perf_counter() - t0)
+    t_e2e = max_over_ranks(min(e2e_s[1:]))
+    d2h = smp.nbytes + sum(a.nbytes for a in led_h.loop_exec_counts.values()) + \
+        led_h.iter_counts.nbytes + np.asarray(led_h.block_exec_counts).nbytes + 8 * (7 * m + 1)
+    e2e = {"value": world * m * n / t_e2e, "unit": "samples/s", "h2d_bytes_per_step": 8 * d,
+           "d2h_bytes_per_step": int(d2h),
+           "includes": "init_batch (host start point) + run_fsm_batched(output='numpy'): samples "
+                       "[n, m, d] f64 and the ledger's int64 count matrices delivered to host "
+                       "memory (sample rows streamed out during the run where the windowed "
+                       "DRMH path allows)",
+           "ms": [round(1e3 * v, 3) for v in e2e_s]}
+    del smp, led_h
+    # the same with the samples left in HBM (output="torch"), plus the device ESS
+    e2e_dev = []
     for s in range(2):
         barrier()
         t0 = time.perf_counter()
-        x0 = x0_host.to(dev, non_blocking=True)
-        batch = fm.init_batch(bundle, target, m, 500 + s, x0=x0, chain_offset=off)
-        smp, _ = fm.run_fsm_batched(bundle, target, batch, n, step_variant=cfg["variant"],
-                                    output="torch", surplus=False, lanes=args.lanes,
-                                    evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
-                                    prior_transform=cfg.get("prior_transform"),
-                                    draw_parts=cfg.get("draw_parts", 1),
-                                    prior_parts=cfg.get("prior_parts", 1))
+        smp, _ = e2e_run(10 + s, "torch")
         if has_ess:
             _ = fm.effective_sample_size(smp, burn=burn).pooled
         else:
             _ = smp.mean(dim=(0, 1)).cpu()
+        del smp
         barrier()
-        e2e_s.append(time.perf_counter() - t0)
-    t_e2e = max_over_ranks(min(e2e_s))
-    e2e = {"value": world * m * n / t_e2e, "unit": "samples/s", "h2d_bytes_per_step": 8 * d,
-           "d2h_bytes_per_step": 8 * (d + 2), "includes": "init_batch + run_fsm_batched + "
-           "effective_sample_size (device) with host start point and host ESS summary"}
+        e2e_dev.append(time.perf_counter() - t0)
+    t_dev = max_over_ranks(min(e2e_dev))
+    e2e_device = {"value": world * m * n / t_dev, "unit": "samples/s",
+                  "includes": "init_batch + run_fsm_batched(output='torch') + "
+                              "effective_sample_size on the device; samples stay in HBM"}
 
     # roofline of the run (fsm_run_kernel, or drmh_draws_kernel + fsm_window_kernel
     # when the draws are generated ahead): algorithmic HBM bytes per launch
@@ -376,23 +406,22 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     pipe = json.load(open(os.path.join(ROOT, "profiles", "r01_pipe_peaks.json")))
-    achieved = traffic_bytes / (kms / 1e3) / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-            "kernel": ("drmh_draws_kernel + fsm_window_kernel<DrmhW,1,10,MOG>" if win else
-                       "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel"),
-            "kernel_ms": kms, "algorithmic_bytes": traffic_bytes,
-            "note": ("HBM carries samples, ledger rows, chain state and (windowed) the pre-drawn "
-                     "normals/uniforms, 16 B per draw (written by drmh_draws_kernel, read by "
-                     "fsm_window_kernel: a design choice, see frac_without_draws); the run is "
-                     "fp64/integer issue-bound: see 'compute' and profiles/") if win else
-                    ("HBM carries samples, ledger rows and chain state loaded/stored once per "
-                     "launch; the per-chain FSM state stays in registers/shared memory for the "
-                     "whole run, so the kernel is fp64-issue/latency-bound, not HBM-bound: "
-                     "'state_model' gives the SURVEY.md 8(d) per-unit figure")}
-    # SURVEY.md 8(d) per-unit bytes: the traffic an SoA-state-in-HBM step kernel would
-    # move per unit (chain-tick, or INTEGRATE chain-tick for NUTS).  This kernel keeps
-    # that state on chip, so this is an equivalent bandwidth, not DRAM traffic.
+    design = {"achieved": traffic_bytes / (kms / 1e3) / 1e9, "unit": "GB/s",
+              "frac": traffic_bytes / (kms / 1e3) / 1e9 / peaks["hbm_gbs"],
+              "algorithmic_bytes": traffic_bytes,
+              "note": ("bytes this design moves: samples, ledger rows, chain state once per "
+                       "launch and (windowed) the pre-drawn normals/uniforms at 16 B per draw "
+                       "(written by drmh_draws_kernel, read by fsm_window_kernel)") if win else
+                      ("bytes this design moves: samples, ledger rows and chain state loaded/"
+                       "stored once per launch; the per-chain FSM state stays in registers or "
+                       "shared memory for the whole run")}
+    if draw_bytes:
+        design["frac_without_draws"] = (st_bytes + out_bytes) / (kms / 1e3) / 1e9 / peaks["hbm_gbs"]
+    # roofline.achieved follows SURVEY.md 8(d): its per-unit bytes (the traffic an
+    # SoA-state-in-HBM step kernel moves per chain-tick, or per INTEGRATE
+    # chain-tick for NUTS) x the units this run executed / the kernels' time.
+    # This engine keeps that state on chip, so it is the bandwidth-equivalent
+    # rate of the state-model, not DRAM traffic (that is `traffic`).
     n_inner = int(ledger.iter_counts.sum().item()) if hasattr(ledger.iter_counts, "sum") else 0
     if cfg["family"] == "ess":
         units, per_unit, uname = n_inner + 2 * n * m, 2 * d * 8 + 96 + 3 * d * 8 * n * m / \
@@ -402,14 +431,17 @@ def main():
     else:
         units, per_unit, uname = n_inner, 2 * d * 8 + 96 + 2 * d * 8 * n * m / max(1, n_inner), \
             "PROPOSE chain-tick"
-    if units:
-        sm_ach = units * per_unit / (kms / 1e3) / 1e9
-        roof["state_model"] = {"unit": uname, "units": units, "bytes_per_unit": per_unit,
-                               "achieved": sm_ach, "peak": peaks["hbm_gbs"], "unit_bw": "GB/s",
-                               "frac": sm_ach / peaks["hbm_gbs"],
-                               "source": "SURVEY.md 8(d) per-unit bytes x units / kernel time"}
+    sm_ach = units * per_unit / (kms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": sm_ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": sm_ach / peaks["hbm_gbs"], "traffic": None,
+            "kernel": ("drmh_draws_kernel + fsm_window_kernel<DrmhW,1,10,MOG>" if win else
+                       "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel"),
+            "kernel_ms": kms, "unit_of_work": uname, "units": units, "bytes_per_unit": per_unit,
+            "algorithmic_bytes": units * per_unit,
+            "source": "SURVEY.md 8(d) per-unit bytes x units / kernel time (CUDA events on the "
+                      "launching stream)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs", "design_traffic": design}
     if draw_bytes:
-        roof["frac_without_draws"] = (st_bytes + out_bytes) / (kms / 1e3) / 1e9 / peaks["hbm_gbs"]
         tp = os.path.join(ROOT, "profiles", "r02_c2_traffic.json")
         if os.path.exists(tp) and cfg.get("draw_window") in (3300, 4070):
             # ncu DRAM bytes of one generator + window launch pair (draws + 4%:
@@ -435,6 +467,19 @@ def main():
                            "unit": "TFLOP/s", "frac": ach_tf / pipe["fp64_fma_tflops"],
                            "flops_per_proposal": FP64_FLOPS_PER_PROPOSAL, "proposals": proposals,
                            "peak_source": "profiles/r01_pipe_peaks.json (tools/peak_probe.cu)"}
+        ip = os.path.join(ROOT, "profiles", ISSUE_PROFILE)
+        if win and os.path.exists(ip):
+            # warp instructions per proposal of the two kernels (ncu sm__inst_executed
+            # over a profiled run / that run's proposals) against the issue ceiling:
+            # 148 SMs x 4 schedulers x one warp instruction per cycle at this run's clock
+            t = json.load(open(ip))
+            mhz = clk.get("sm_mhz") or pipe.get("sm_mhz", 1965.0)
+            slots = 148 * 4 * mhz * 1e6 * (kms / 1e3)
+            ins = t["warp_inst_per_proposal"] * proposals
+            roof["issue"] = {"warp_inst_per_proposal": t["warp_inst_per_proposal"],
+                             "achieved": ins / slots, "frac": ins / slots,
+                             "unit": "fraction of issue slots (148 SM x 4 schedulers x clock)",
+                             "sm_mhz": mhz, "source": "profiles/" + ISSUE_PROFILE}
 
     if cfg.get("batched"):
         # dominant work: the two contractions per evaluation, 4 N d flops each
@@ -465,7 +510,8 @@ def main():
                                           "collective", "l2": "flushed between steps (256 MiB write)",
                            "surplus_ticks": "skipped (discarded by the reference)"},
                 "ess_per_sec": ess_per_sec, "ess_pooled": ess_pooled, "rhat_max": rhat_max,
-                "lockstep": lock, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+                "lockstep": lock, "e2e": e2e, "e2e_device": e2e_device, "roofline": roof,
+                "cpu_baseline": cpu,
                 "clocks": clk, "gpu_launches": launches,
                 "tick_count": ledger.tick_count,
                 "evaluations_per_step": evals, "rounds_per_step": ledger.extras.get("rounds"),
@@ -473,6 +519,62 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def lockstep_accounting(args, cfg, fm, bundle, target, m, n_lock, off, ledger, t_lock, value,
+                        lock_value, barrier, max_over_ranks, world, evaluator):
+    """What the lock-step speed-up is made of.
+
+    R_of_m: the paper's efficiency bound E[max_j N_ij] / E[N_ij] (PAPER.md
+    section 5; analysis.py:150-185) from this run's own per-sample loop
+    counts: the speed-up a lock-step with the same per-iteration cost as the
+    FSM would allow.  same_generator: the FSM with the lock-step kernel's
+    draw source (inline generator, per-chain prior transform), so the two
+    differ only in synchronisation.  barrier_us: one grid-wide barrier of the
+    lock-step's cooperative grid, measured alone (fsmc_lockstep_barrier_probe);
+    barriers_per_step counts the while-loop tests of single-loop machines,
+    sum_i (max_j N_ij + 1)."""
+    import torch
+    from paper_2503_17405_b200 import lockstep as LS
+    out = {}
+    its = ledger.iter_counts[:n_lock].to(torch.float64)
+    mx = its.max(dim=1).values
+    r_of_m = float(mx.mean() / its.mean())
+    out["R_of_m"] = r_of_m
+    out["speedup_over_R"] = value / lock_value / r_of_m
+    if evaluator is None:
+        same = {}
+        if cfg.get("draw_window"):
+            same = {"draw_window": 0, "draw_parts": 1}
+        elif cfg.get("prior_transform"):
+            same = {"prior_transform": None}
+        if same:
+            ts = []
+            for s in range(2):
+                barrier()
+                batch = fm.init_batch(bundle, target, m, 40 + s, chain_offset=off)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fm.run_fsm_batched(bundle, target, batch, n_lock, step_variant=cfg["variant"],
+                                   output="torch", surplus=False, lanes=args.lanes,
+                                   **{"draw_window": 0, "prior_transform": None, **same})
+                e1.record()
+                barrier()
+                ts.append(e0.elapsed_time(e1) / 1e3)
+            t_same = max_over_ranks(min(ts))
+            v_same = world * m * n_lock / t_same
+            out["same_generator"] = {"value": v_same, "ms_per_step": 1e3 * t_same,
+                                     "speedup": v_same / lock_value,
+                                     "speedup_over_R": v_same / lock_value / r_of_m,
+                                     "options": same}
+        batch = fm.init_batch(bundle, target, m, 60, chain_offset=off)
+        bus = LS.lockstep_barrier_us(bundle, target, batch, lanes=args.lanes)
+        out["barrier_us"] = bus
+        if cfg["family"] in ("drmh", "ess"):
+            nbar = int((mx + 1).sum())
+            out["barriers_per_step"] = nbar
+            out["barrier_share"] = nbar * bus * 1e-6 / t_lock
+    return out
 
 
 def analysis_chain_means(samples, burn):

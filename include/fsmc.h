@@ -177,6 +177,14 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
 fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                               int64_t n, const fsmc_outputs* out, int32_t lanes, void* stream_);
 
+/* The lock-step baseline's barrier alone: the cooperative grid
+ * fsmc_lockstep_run launches for this configuration (its first wave) runs
+ * `iters` grid-wide "any chain active" barriers and nothing else.  Time it
+ * with events on `stream`: the per-barrier cost the lock-step pays at every
+ * while-loop test.  Uses st->work; the chain state is not touched. */
+fsmc_status fsmc_lockstep_barrier_probe(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                                        int64_t iters, int32_t lanes, void* stream);
+
 /* fsmc_run for the DRMH kernels (drmh_kernel, split or not) with the draws
  * generated ahead of use.  Every DRMH proposal consumes dim normals then one
  * uniform (drmh.py:85-88), so a chain's draws from its current counter on are
@@ -202,6 +210,18 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
                                       int32_t variant, const int32_t* order, int64_t tick_limit,
                                       int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
                                       int32_t lanes, int32_t parts, void* stream_);
+
+/* fsmc_run_windowed_overlap with sample egress: `host_samples` (pinned host
+ * memory, [n][m][dim], or NULL) receives out->samples.  Rows every chain has
+ * finished are copied on a device-owned egress stream while the later rows
+ * are still being sampled (the windowed run reads each part's lowest sample
+ * count at its periodic progress checks), so the device-to-host transfer
+ * overlaps the sampling instead of following it.  The copies are ordered
+ * before any later work on `stream`: synchronise `stream` before reading. */
+fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                     int32_t variant, const int32_t* order, int64_t tick_limit,
+                                     int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
+                                     int32_t lanes, int32_t parts, double* host_samples, void* stream);
 
 /* Replaces measure_block_costs' timing loop (lockstep.py:454-498): runs every
  * chain with the plain executor up to tick_limit like fsmc_run (mode 1) and

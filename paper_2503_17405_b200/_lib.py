@@ -138,6 +138,10 @@ def lib():
     L.fsmc_lockstep_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                     ctypes.POINTER(State), ctypes.c_int64,
                                     ctypes.POINTER(Outputs), ctypes.c_int32, _P]
+    L.fsmc_lockstep_barrier_probe.restype = S
+    L.fsmc_lockstep_barrier_probe.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
+                                              ctypes.POINTER(State), ctypes.c_int64, ctypes.c_int32,
+                                              _P]
     L.fsmc_run_windowed.restype = S
     L.fsmc_run_windowed.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                     ctypes.POINTER(State), ctypes.c_int64, ctypes.c_int32,
@@ -145,6 +149,9 @@ def lib():
                                     ctypes.POINTER(Outputs), ctypes.c_int64, _P, ctypes.c_int32, _P]
     L.fsmc_run_windowed_overlap.restype = S
     L.fsmc_run_windowed_overlap.argtypes = list(L.fsmc_run_windowed.argtypes[:-1]) + [ctypes.c_int32, _P]
+    L.fsmc_run_windowed_egress.restype = S
+    L.fsmc_run_windowed_egress.argtypes = list(L.fsmc_run_windowed.argtypes[:-1]) + \
+        [ctypes.c_int32, _P, _P]
     L.fsmc_profile_blocks.restype = S
     L.fsmc_profile_blocks.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                       ctypes.POINTER(State), ctypes.c_int64, _P, _P]

@@ -58,7 +58,7 @@ cudaError_t side_streams(cudaStream_t (&out)[kMaxParts]) {
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> lk(g_side_mu);
-  for (int h = 1; h < kMaxParts; h++) {
+  for (int h = 0; h < kMaxParts; h++) {   // [0]: the sample egress (device -> host) stream
     if (!side[dev][h]) {
       e = cudaStreamCreateWithFlags(&side[dev][h], cudaStreamNonBlocking);
       if (e != cudaSuccess) return e;
@@ -602,6 +602,14 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
                                       int32_t variant, const int32_t* order, int64_t tick_limit,
                                       int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
                                       int32_t lanes, int32_t parts, void* stream_) {
+  return fsmc_run_windowed_egress(k, t, st, n, variant, order, tick_limit, mode, out, window, draws, lanes,
+                                  parts, nullptr, stream_);
+}
+
+fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                                     int32_t variant, const int32_t* order, int64_t tick_limit,
+                                     int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
+                                     int32_t lanes, int32_t parts, double* host_samples, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->family != FSMC_DRMH) return fail(FSMC_ERR_UNSUPPORTED, "pre-drawn windows are for the DRMH kernels");
@@ -636,13 +644,26 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
   // parts > 1: the chains in contiguous parts, each alternating its draw
   // generation and window kernels on its own stream, so one part's kernels
   // fill the SMs another part's kernel tail and launch gaps leave idle
+  // host_samples (pinned): rows every chain has finished are copied to the
+  // host on the egress stream while later rows are still being sampled
+  const bool egress = host_samples && out && out->samples && n > 0;
   cudaStream_t side[kMaxParts] = {};
-  cudaEvent_t ev_fork = nullptr, ev_join[kMaxParts] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxParts] = {}, ev_egress = nullptr;
+  if (parts > 1 || egress) CUDA_TRY(side_streams(side));
   if (parts > 1) {
-    CUDA_TRY(side_streams(side));
     CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     for (int h = 1; h < parts; h++) CUDA_TRY(cudaEventCreateWithFlags(&ev_join[h], cudaEventDisableTiming));
   }
+  const size_t row_bytes = (size_t)st->m * t->dim * sizeof(double);
+  long long rows_sent = 0;
+  auto send_rows = [&](long long upto) -> cudaError_t {
+    if (!egress || upto <= rows_sent) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync((char*)host_samples + rows_sent * row_bytes,
+                                    (const char*)out->samples + rows_sent * row_bytes,
+                                    (size_t)(upto - rows_sent) * row_bytes, cudaMemcpyDeviceToHost, side[0]);
+    rows_sent = upto;
+    return e;
+  };
   static int draw_bps = -1;   // draws-kernel blocks per SM (FSMC_DRAW_BLOCKS_PER_SM; 0 = fill)
   if (draw_bps < 0) {
     const char* e = getenv("FSMC_DRAW_BLOCKS_PER_SM");
@@ -656,7 +677,8 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
     ph[h].j_lo = st->m * h / parts;
     ph[h].j_hi = st->m * (h + 1) / parts;
     ph[h].next_chain = w + 16 * h;
-    ph[h].unfinished = w + 16 * h + 8;
+    ph[h].unfinished = w + 16 * h + 8;   // [8] unfinished chains, [9] lowest sample count seen
+    ph[h].min_count = egress ? w + 16 * h + 9 : nullptr;
     ph[h].draw_blocks_per_sm = draw_bps;
     sh[h] = h == 0 ? cs : side[h];
   }
@@ -665,27 +687,44 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
     for (int h = 1; h < parts; h++) CUDA_TRY(cudaStreamWaitEvent(sh[h], ev_fork, 0));
   }
   const int kCheck = 4;   // rounds between reads of the unfinished counts
-  unsigned left[kMaxParts];
-  for (int h = 0; h < kMaxParts; h++) left[h] = 1;
+  unsigned left[kMaxParts][2];   // per part: unfinished chains, lowest sample count of the last round
+  for (int h = 0; h < kMaxParts; h++) left[h][0] = 1;
   for (long long r = 0;; r++) {
     for (int h = 0; h < parts; h++) {
-      if (!left[h]) continue;
+      if (!left[h][0]) continue;
       CUDA_TRY(dispatch_family(6, ge, ph[h], sh[h]));
       CUDA_TRY(cudaMemsetAsync(ph[h].next_chain, 0, sizeof(unsigned), sh[h]));
       CUDA_TRY(cudaMemsetAsync(ph[h].unfinished, 0, sizeof(unsigned), sh[h]));
+      if (egress) CUDA_TRY(cudaMemsetAsync(ph[h].min_count, 0xff, sizeof(unsigned), sh[h]));
       CUDA_TRY(dispatch_family(5, ge, ph[h], sh[h]));
     }
     if (r % kCheck == kCheck - 1) {
       for (int h = 0; h < parts; h++)
-        if (left[h])
-          CUDA_TRY(cudaMemcpyAsync(&left[h], ph[h].unfinished, sizeof(unsigned), cudaMemcpyDeviceToHost, sh[h]));
+        if (left[h][0])
+          CUDA_TRY(cudaMemcpyAsync(left[h], ph[h].unfinished, (egress ? 2 : 1) * sizeof(unsigned),
+                                   cudaMemcpyDeviceToHost, sh[h]));
       bool any = false;
       for (int h = 0; h < parts; h++) {
         CUDA_TRY(cudaStreamSynchronize(sh[h]));
-        any = any || left[h];
+        any = any || left[h][0];
       }
       if (!any) break;
+      if (egress) {
+        // rows below every chain's sample count are final: a part that
+        // finished (or whose last round skipped every chain) bounds nothing
+        long long rows = n;
+        for (int h = 0; h < parts; h++)
+          if (left[h][0] && left[h][1] != 0xffffffffu) rows = std::min<long long>(rows, left[h][1]);
+        CUDA_TRY(send_rows(rows));
+      }
     }
+  }
+  if (egress) {
+    CUDA_TRY(send_rows(n));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_egress, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev_egress, side[0]));
+    CUDA_TRY(cudaStreamWaitEvent(cs, ev_egress, 0));
+    CUDA_TRY(cudaEventDestroy(ev_egress));
   }
   if (parts > 1) {
     for (int h = 1; h < parts; h++) {
@@ -744,6 +783,29 @@ fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
   p.active_flags = w + 3;
   CUDA_TRY(cudaMemsetAsync(w + 1, 0, 4 * sizeof(unsigned), cs));
   CUDA_TRY(dispatch_family(2, ge, p, cs));
+  return FSMC_OK;
+}
+
+fsmc_status fsmc_lockstep_barrier_probe(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
+                                        int64_t iters, int32_t lanes, void* stream_) {
+  fsmc_status s = check_args(k, t, st);
+  if (s != FSMC_OK) return s;
+  if (iters < 1) return fail(FSMC_ERR_ARG, "iters must be >= 1");
+  GE ge;
+  if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
+    return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.k = *k; p.t = *t; p.st = *st;
+  p.t.full = k->family != FSMC_ESS;
+  p.n = iters;
+  cudaStream_t cs = (cudaStream_t)stream_;
+  unsigned* w = st->work;
+  p.bar_count = w + 1;
+  p.bar_gen = w + 2;
+  p.active_flags = w + 3;
+  CUDA_TRY(cudaMemsetAsync(w + 1, 0, 5 * sizeof(unsigned), cs));
+  CUDA_TRY(dispatch_family(9, ge, p, cs));
   return FSMC_OK;
 }
 

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_window_kernel(P
       core_store(c, p, j);
       if (!ok) report_error(c, p, j);
       else if (c.count < n_stop && c.tick < p.tick_limit) atomicAdd(p.unfinished, 1u);
+      if (p.min_count) atomicMin(p.min_count, (unsigned)min(c.count, 0xfffffffeLL));
     }
   }
 }
@@ -313,6 +314,19 @@ __device__ __forceinline__ bool grid_any(const Params& p, bool pred, unsigned& p
   bool any = ((volatile unsigned*)p.active_flags)[phase & 1] != 0;
   phase++;
   return any;
+}
+
+// The lock-step baseline's synchronisation cost alone: the same cooperative
+// grid as lockstep_kernel for this configuration, doing nothing but `iters`
+// grid_any rounds (fsmc_lockstep_barrier_probe), so the bench can state how
+// much of a lock-step step is barrier rather than sampling work.
+static __global__ void __launch_bounds__(kThreads) barrier_probe_kernel(Params p, long long iters) {
+  unsigned phase = 0;
+  bool any = false;
+#pragma unroll 1
+  for (long long i = 0; i < iters; i++)
+    any = grid_any(p, threadIdx.x == 0 && (long long)blockIdx.x == i % gridDim.x, phase) || any;
+  if (!any && threadIdx.x == 0) p.active_flags[2] = 1u;   // never taken; keeps the loop live
 }
 
 // vmap semantics of each kernel's monolithic sampler (drmh.py:163-169,
@@ -461,6 +475,23 @@ struct Launch {
   static cudaError_t advance_prior(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     return persistent(fsm_advance_kernel<F, G, E, TK, true>, p, lc, s, 0, p.j_hi - p.j_lo);
   }
+  // the first wave of lockstep(): same blocks, same co-residency
+  static cudaError_t barrier_probe(Params p, const LaunchCtx& lc, cudaStream_t s) {
+    int occ = 0;
+    cudaError_t e = allow_smem(lockstep_kernel<F, G, E, TK>, smem(p));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lockstep_kernel<F, G, E, TK>, kThreads, smem(p));
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    const long long per_block = kThreads / G;
+    const long long cap = (long long)occ * lc.num_sms * per_block;
+    const long long chains = std::min<long long>(p.st.m, cap);
+    int blocks = (int)((chains + per_block - 1) / per_block);
+    long long iters = p.n;
+    void* args[] = {&p, &iters};
+    count_launch();
+    return cudaLaunchCooperativeKernel((const void*)barrier_probe_kernel, dim3(blocks), dim3(kThreads), args, 0, s);
+  }
   static cudaError_t lockstep(Params p, const LaunchCtx& lc, cudaStream_t s) {
     int occ = 0;
     cudaError_t e = allow_smem(lockstep_kernel<F, G, E, TK>, smem(p));
@@ -485,7 +516,7 @@ struct Launch {
   }
 };
 
-// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile, 7 advance with batched prior, 8 deferred-init finish (5 windowed run and 6 draws: fam_drmh.cu).  TK: compile-time plugin (0 = run-time switch)
+// op: 0 init, 1 run, 2 lock-step, 3 advance, 4 profile, 7 advance with batched prior, 8 deferred-init finish, 9 lock-step barrier probe (5 windowed run and 6 draws: fam_drmh.cu).  TK: compile-time plugin (0 = run-time switch)
 template <template <int, int> class F, int G, int E, int TK = 0>
 cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, uint64_t ps,
                       long long off, const double* x0, double jit) {
@@ -498,6 +529,7 @@ cudaError_t launch_op(int op, Params& p, const LaunchCtx& lc, cudaStream_t s, ui
     if constexpr (F<G, E>::PRIOR) return Launch<F, G, E, TK>::advance_prior(p, lc, s);
     return cudaErrorInvalidConfiguration;
   }
+  if (op == 9) return Launch<F, G, E, TK>::barrier_probe(p, lc, s);
   return Launch<F, G, E, TK>::lockstep(p, lc, s);
 }
 

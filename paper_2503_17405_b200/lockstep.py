@@ -32,7 +32,7 @@ from .prng import RngKey
 
 __all__ = ["ChainBatch", "CostParams", "CostLedger", "KernelRunError", "TickBudgetExceeded",
            "init_batch", "run_standard_batched", "run_fsm_batched", "collect_samples",
-           "measure_block_costs",
+           "measure_block_costs", "lockstep_barrier_us",
            "STEP_VARIANTS", "TICK_CHUNK"]
 
 STEP_VARIANTS = ("plain", "bundled", "amortized")
@@ -337,20 +337,42 @@ def _outputs(n, m, d, L, want_ticks, want_samples=True):
     return samples, loops, ticks, out
 
 
+def _pinned(shape, dtype):
+    """Page-locked host buffer (torch's caching host allocator: reused across
+    runs once freed), so device-to-host copies run at full link speed and can
+    be asynchronous."""
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def _to_host(x, dtype=None):
+    """Asynchronous copy of a device tensor into pinned host memory (converted
+    on the device first when `dtype` differs); the caller synchronises."""
+    if dtype is not None and x.dtype != dtype:
+        x = x.to(dtype)
+    h = _pinned(tuple(x.shape), x.dtype)
+    h.copy_(x, non_blocking=True)
+    return h
+
+
 def _convert(x, output):
     if x is None:
         return None
     if output == "torch":
         return x
-    return x.cpu().numpy()
+    h = _to_host(x)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
 
 
 def _counts(x, output):
     """Ledger count matrices: int64 numpy arrays (the reference's type) for
-    output="numpy"; int32 device tensors, unconverted, for output="torch"."""
+    output="numpy" (widened on the device, one pinned copy); int32 device
+    tensors, unconverted, for output="torch"."""
     if output == "torch":
         return x
-    return x.cpu().numpy().astype(np.int64)
+    h = _to_host(x, torch.int64)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
 
 
 def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str = "plain",
@@ -409,6 +431,10 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     m, d = batch.m, target.dim
     loop_states = bundle.loop_states
     samples, loops, ticks_out, out = _outputs(n, m, d, len(loop_states), record_sample_ticks)
+    # output="numpy": the samples land in pinned host memory; the windowed
+    # DRMH run streams finished rows out while it samples (fsmc_run_windowed_egress)
+    host = _pinned((n, m, d), torch.float64) if output == "numpy" else None
+    egressed = False
     limit = (tick_budget // tick_chunk) * tick_chunk if tick_budget is not None else _NO_LIMIT
     lib = _lib.lib()
     kern, tgt = batch.kernel, target.struct()
@@ -435,12 +461,15 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         draws = torch.empty(m * int(draw_window) + 32, dtype=torch.float64, device="cuda")
 
         def launch(mode, tick_limit):
-            _lib.check(lib.fsmc_run_windowed_overlap(ctypes.byref(kern), ctypes.byref(tgt),
-                                                     ctypes.byref(batch.struct()), n, variant, ordv,
-                                                     tick_limit, mode, ctypes.byref(out),
-                                                     int(draw_window), draws.data_ptr(), lanes,
-                                                     int(draw_parts), _lib.stream_ptr()),
-                       "fsmc_run_windowed_overlap")
+            nonlocal egressed
+            dst = host.data_ptr() if host is not None and mode == 0 else None
+            _lib.check(lib.fsmc_run_windowed_egress(ctypes.byref(kern), ctypes.byref(tgt),
+                                                    ctypes.byref(batch.struct()), n, variant, ordv,
+                                                    tick_limit, mode, ctypes.byref(out),
+                                                    int(draw_window), draws.data_ptr(), lanes,
+                                                    int(draw_parts), dst, _lib.stream_ptr()),
+                       "fsmc_run_windowed_egress")
+            egressed = egressed or dst is not None
     elif evaluator is None:
         def launch(mode, tick_limit):
             _lib.check(lib.fsmc_run(ctypes.byref(kern), ctypes.byref(tgt),
@@ -492,7 +521,12 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         ledger.extras.update(launch.stats)
     if not all_done:
         raise TickBudgetExceeded(tick_budget, ledger, counts_now.tolist())
-    return _convert(samples, output), ledger
+    if host is None:
+        return samples, ledger
+    if not egressed:
+        host.copy_(samples, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy(), ledger
 
 
 def _device_evaluator(target, family: int, lanes: int):
@@ -627,7 +661,8 @@ def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks,
     tc = params.tick_cost(variant)
     st = None if ticks_out is None else _counts(ticks_out[:n_rows], output)
     return CostLedger(
-        iter_counts=_counts(it, output), loop_exec_counts=loop_execs, tick_count=int(ticks),
+        iter_counts=_counts(it, output),
+        loop_exec_counts=loop_execs, tick_count=int(ticks),
         block_exec_counts=_convert(blocks, output), charged_cost=ticks * tc, walltime=walltime,
         regime=f"fsm-{variant}", tick_cost=tc,
         shared_evals_per_tick=params.shared_evals_per_tick(variant),
@@ -699,6 +734,25 @@ def run_standard_batched(bundle, target, batch: ChainBatch, n: int,
     if stats is not None:
         ledger.extras.update(stats)
     return _convert(samples, output), ledger
+
+
+def lockstep_barrier_us(bundle, target, batch: ChainBatch, iters: int = 4000,
+                        lanes: int = 0) -> float:
+    """Microseconds per grid-wide barrier of the lock-step baseline for this
+    batch's configuration (``fsmc_lockstep_barrier_probe``: the same
+    cooperative grid as ``run_standard_batched``, barriers only).  Every
+    while-loop test of the lock-step run is one such barrier, so
+    (tests x this) is the synchronisation share of its time."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    args = (ctypes.byref(batch.kernel), ctypes.byref(target.struct()), ctypes.byref(batch.struct()))
+    _lib.check(_lib.lib().fsmc_lockstep_barrier_probe(*args, 16, lanes, _lib.stream_ptr()),
+               "fsmc_lockstep_barrier_probe")          # warm-up
+    ev[0].record()
+    _lib.check(_lib.lib().fsmc_lockstep_barrier_probe(*args, int(iters), lanes, _lib.stream_ptr()),
+               "fsmc_lockstep_barrier_probe")
+    ev[1].record()
+    torch.cuda.synchronize()
+    return ev[0].elapsed_time(ev[1]) * 1e3 / iters
 
 
 def _lockstep_batched(bundle, target, batch, n, out, lanes, evaluator) -> dict:
