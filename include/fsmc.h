@@ -337,6 +337,12 @@ fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, i
 fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16, const void* x_bf16,
                                 const void* xt_bf16, const double* xty, int64_t n_obs, int64_t dim,
                                 double* lp, double* grad, void* stream_);
+/* The same with the operand type chosen: operand 0 = bf16 (as above), 1 =
+ * fp16 (11-bit mantissa: theta is rounded ~8x more finely, the same tensor
+ * issue rate); theta_h16 / x_h16 / xt_h16 then hold fp16. */
+fsmc_status fsmc_logreg_tc_eval2(const double* theta, int64_t k, void* theta_h16, const void* x_h16,
+                                 const void* xt_h16, const double* xty, int64_t n_obs, int64_t dim,
+                                 double* lp, double* grad, int32_t operand, void* stream_);
 const char* fsmc_logreg_tc_last_error(void);
 
 /* Batched GP-hyperparameter marginal likelihood (targets.py:191-265) for k

@@ -163,6 +163,9 @@ def lib():
     L.fsmc_logreg_tc_eval.restype = S
     L.fsmc_logreg_tc_eval.argtypes = [_P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64,
                                       ctypes.c_int64, _P, _P, _P]
+    L.fsmc_logreg_tc_eval2.restype = S
+    L.fsmc_logreg_tc_eval2.argtypes = [_P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64,
+                                       ctypes.c_int64, _P, _P, ctypes.c_int32, _P]
     L.fsmc_logreg_tc_last_error.restype = ctypes.c_char_p
     L.fsmc_diag_partials.restype = S
     L.fsmc_diag_partials.argtypes = [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,

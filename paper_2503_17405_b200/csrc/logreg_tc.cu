@@ -23,6 +23,7 @@
 // S is double-buffered in TMEM so the epilogue of tile i overlaps MMA1 of i+1.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -98,10 +99,36 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;             // SWIZZLE_128B
   return d;
 }
-// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, both K-major
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// kind::f16 instruction descriptor: 16-bit operands (format 1 = bf16, 0 =
+// fp16) -> fp32 accumulator, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, uint32_t fmt) {
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// operand element type: bf16 (8-bit mantissa) or fp16 (11-bit mantissa, the
+// same issue rate; the design entries N(0,1)/sqrt(d) and sigmoid values in
+// [0,1] sit well inside its range)
+template <bool F16>
+struct Op;
+template <>
+struct Op<false> {
+  using T = __nv_bfloat16;
+  static constexpr uint32_t fmt = 1;
+  __device__ static uint32_t pack(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+  __device__ static T from(float a) { return __float2bfloat16_rn(a); }
+};
+template <>
+struct Op<true> {
+  using T = __half;
+  static constexpr uint32_t fmt = 0;
+  __device__ static uint32_t pack(float a, float b) {
+    __half2 v = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+  __device__ static T from(float a) { return __float2half_rn(a); }
+};
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -134,6 +161,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+template <bool F16>
 __global__ void __launch_bounds__(NTHREADS, 1)
     logreg_tc_kernel(const __grid_constant__ CUtensorMap map_theta, const __grid_constant__ CUtensorMap map_x,
                      const __grid_constant__ CUtensorMap map_xt, const double* __restrict__ xty,
@@ -199,8 +227,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // --------------------------------------------- MMA issuer
-      constexpr uint32_t ID1 = idesc_bf16(BM, BN);
-      constexpr uint32_t ID2 = idesc_bf16(BM, DF);
+      constexpr uint32_t ID1 = idesc_f16(BM, BN, Op<F16>::fmt);
+      constexpr uint32_t ID2 = idesc_f16(BM, DF, Op<F16>::fmt);
       mbar_wait(bar(B_THETA), 0);
       tc_fence_after();
       auto mma2 = [&](int i) {  // G += R_i X_i  (K = 64 rows of tile i)
@@ -273,8 +301,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           float rv[2];
 #pragma unroll
           for (int h = 0; h < 2; h++) acc[(c + h) & 3] += element(z[c + h], rv[h]);
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(rv[0], rv[1]);
-          packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+          packed[c >> 1] = Op<F16>::pack(rv[0], rv[1]);
         }
       } else {
 #pragma unroll
@@ -285,8 +312,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const float sp = element(z[c + h], rv[h]);
             acc[(c + h) & 3] += (c + h) < valid ? sp : 0.0f;   // rows past N have x = 0: no G term
           }
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(rv[0], rv[1]);
-          packed[c >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+          packed[c >> 1] = Op<F16>::pack(rv[0], rv[1]);
         }
       }
       lp_acc += (double)((acc[0] + acc[1]) + (acc[2] + acc[3]));
@@ -340,12 +366,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-// fp64 chain positions -> bf16 rows (padded to a multiple of 128 with zeros)
-__global__ void to_bf16_kernel(const double* __restrict__ src, long long rows, long long rows_pad,
-                               __nv_bfloat16* __restrict__ dst) {
+// fp64 chain positions -> 16-bit rows (padded to a multiple of 128 with zeros)
+template <bool F16>
+__global__ void to_half_kernel(const double* __restrict__ src, long long rows, long long rows_pad,
+                               typename Op<F16>::T* __restrict__ dst) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= rows_pad * DF) return;
-  dst[i] = __float2bfloat16_rn(i < rows * DF ? (float)src[i] : 0.0f);
+  dst[i] = Op<F16>::from(i < rows * DF ? (float)src[i] : 0.0f);
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -364,15 +391,15 @@ EncodeTiled encoder() {
   return fn;
 }
 
-// 2-D bf16 tensor [rows][cols] (row-major), box [box_rows][64 cols], SWIZZLE_128B
-bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// 2-D 16-bit tensor [rows][cols] (row-major), box [box_rows][64 cols], SWIZZLE_128B
+bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows, bool f16) {
   EncodeTiled enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -385,40 +412,51 @@ extern "C" {
 
 const char* fsmc_logreg_tc_last_error(void) { return g_err.c_str(); }
 
-/* Fused tcgen05 logistic-regression evaluation (see fsmc.h). */
-fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16, const void* x_bf16,
-                                const void* xt_bf16, const double* xty, int64_t n_obs, int64_t dim, double* lp,
-                                double* grad, void* stream_) {
+/* Fused tcgen05 logistic-regression evaluation (see fsmc.h).  operand: 0 =
+ * bf16, 1 = fp16 (theta_h16 / x_h16 / xt_h16 then hold that type). */
+fsmc_status fsmc_logreg_tc_eval2(const double* theta, int64_t k, void* theta_h16, const void* x_h16,
+                                 const void* xt_h16, const double* xty, int64_t n_obs, int64_t dim, double* lp,
+                                 double* grad, int32_t operand, void* stream_) {
   if (dim != DF) { g_err = "fused logistic-regression kernel is compiled for d = 256"; return FSMC_ERR_UNSUPPORTED; }
-  if (!theta || !theta_bf16 || !x_bf16 || !xt_bf16 || !xty || !lp || !grad || k < 0 || n_obs < 1) {
+  if (!theta || !theta_h16 || !x_h16 || !xt_h16 || !xty || !lp || !grad || k < 0 || n_obs < 1 ||
+      (operand != 0 && operand != 1)) {
     g_err = "bad arguments";
     return FSMC_ERR_ARG;
   }
   if (!k) return FSMC_OK;
+  const bool f16 = operand == 1;
   cudaStream_t s = (cudaStream_t)stream_;
   const long long kpad = (k + BM - 1) / BM * BM;
-  fsmc::count_launch(2);   // this and logreg_tc_kernel
-  to_bf16_kernel<<<(unsigned)((kpad * DF + 255) / 256), 256, 0, s>>>(theta, k, kpad, (__nv_bfloat16*)theta_bf16);
+  fsmc::count_launch(2);   // the conversion and logreg_tc_kernel
+  const unsigned cb = (unsigned)((kpad * DF + 255) / 256);
+  if (f16) to_half_kernel<true><<<cb, 256, 0, s>>>(theta, k, kpad, (__half*)theta_h16);
+  else to_half_kernel<false><<<cb, 256, 0, s>>>(theta, k, kpad, (__nv_bfloat16*)theta_h16);
   CUtensorMap mt, mx, mxt;
-  if (!make_map(&mt, theta_bf16, kpad, DF, BM) || !make_map(&mx, x_bf16, n_obs, DF, BN) ||
-      !make_map(&mxt, xt_bf16, DF, n_obs, DF)) {
+  if (!make_map(&mt, theta_h16, kpad, DF, BM, f16) || !make_map(&mx, x_h16, n_obs, DF, BN, f16) ||
+      !make_map(&mxt, xt_h16, DF, n_obs, DF, f16)) {
     g_err = "cuTensorMapEncodeTiled failed (alignment: n_obs must be a multiple of 8)";
     return FSMC_ERR_ARG;
   }
   // the shared-memory opt-in is a per-device function attribute
-  static bool attr[64] = {};
+  static bool attr[2][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || !attr[dev]) {
-    cudaError_t ea = cudaFuncSetAttribute(logreg_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  auto kern = f16 ? logreg_tc_kernel<true> : logreg_tc_kernel<false>;
+  if (dev < 0 || dev >= 64 || !attr[f16][dev]) {
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (ea != cudaSuccess) { g_err = cudaGetErrorString(ea); return FSMC_ERR_CUDA; }
-    if (dev >= 0 && dev < 64) attr[dev] = true;
+    if (dev >= 0 && dev < 64) attr[f16][dev] = true;
   }
-  logreg_tc_kernel<<<(unsigned)(kpad / BM), NTHREADS, SMEM_BYTES, s>>>(mt, mx, mxt, xty, theta, k, n_obs, lp,
-                                                                      grad);
+  kern<<<(unsigned)(kpad / BM), NTHREADS, SMEM_BYTES, s>>>(mt, mx, mxt, xty, theta, k, n_obs, lp, grad);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return FSMC_ERR_CUDA; }
   return FSMC_OK;
+}
+
+fsmc_status fsmc_logreg_tc_eval(const double* theta, int64_t k, void* theta_bf16, const void* x_bf16,
+                                const void* xt_bf16, const double* xty, int64_t n_obs, int64_t dim, double* lp,
+                                double* grad, void* stream_) {
+  return fsmc_logreg_tc_eval2(theta, k, theta_bf16, x_bf16, xt_bf16, xty, n_obs, dim, lp, grad, 0, stream_);
 }
 
 }  // extern "C"

@@ -15,10 +15,14 @@ Bayesian logistic regression (``targets.logistic_regression_target``):
 ``precision="fp64"`` evaluates in IEEE double (parity with the per-chain
 plugin up to reduction order).  ``"tf32"`` runs both contractions as cuBLAS
 TF32 GEMMs with the σ / softplus / row-sum epilogue in one pass over Z
-(``fsmc_logreg_epilogue``).  ``"bf16-tc"`` is the fused hand-written tcgen05
-kernel (``csrc/logreg_tc.cu``, d = 256): bf16 operands by TMA, both products
-accumulated in TMEM, the logits never stored.  The reduced precisions give
-distributional parity only.  Chains are processed in tiles so a
+(``fsmc_logreg_epilogue``).  ``"bf16-tc"`` / ``"fp16-tc"`` are the fused
+hand-written tcgen05 kernel (``csrc/logreg_tc.cu``, d = 256): 16-bit operands
+by TMA, both products accumulated in fp32 in TMEM, the logits never stored.
+fp16 carries 11 mantissa bits to bf16's 8 at the same tensor rate, so theta
+is rounded 8x more finely: at N = 100k the log density is the sum of 1e5
+terms, and its error from rounding theta scales with N (tests/
+test_gpu_distribution.py).  The reduced precisions give distributional
+parity only.  Chains are processed in tiles so a
 materialised Z never exceeds ``tile`` rows.
 """
 
@@ -33,8 +37,8 @@ __all__ = ["LogisticRegressionEvaluator"]
 
 class LogisticRegressionEvaluator:
     def __init__(self, X, y, precision: str = "fp64", tile: int = 4096):
-        if precision not in ("fp64", "tf32", "bf16-tc"):
-            raise ValueError("precision must be fp64, tf32 or bf16-tc")
+        if precision not in ("fp64", "tf32", "bf16-tc", "fp16-tc"):
+            raise ValueError("precision must be fp64, tf32, bf16-tc or fp16-tc")
         self.precision = precision
         self.tile = int(tile)
         X = torch.as_tensor(X, dtype=torch.float64, device="cuda").contiguous()
@@ -49,15 +53,17 @@ class LogisticRegressionEvaluator:
             if d != 256 or n % 8:
                 raise ValueError("the fused kernel needs d = 256 and n_obs a multiple of 8")
             self.n_obs, self.d = n, d
-            self.Xb = X.to(torch.bfloat16).contiguous()
+            self.h16 = torch.float16 if precision == "fp16-tc" else torch.bfloat16
+            self.operand = 1 if precision == "fp16-tc" else 0
+            self.Xb = X.to(self.h16).contiguous()
             self.XTb = self.Xb.T.contiguous()
             self.xty = (X.T @ y).contiguous()     # label terms, linear in theta (fp64)
-            self.theta_b = torch.empty(0, dtype=torch.bfloat16, device="cuda")
+            self.theta_b = torch.empty(0, dtype=self.h16, device="cuda")
 
     def __call__(self, theta: torch.Tensor, lp: torch.Tensor, grad: torch.Tensor | None):
         if self.precision == "fp64":
             return self._fp64(theta, lp, grad)
-        if self.precision == "bf16-tc":
+        if self.precision in ("bf16-tc", "fp16-tc"):
             return self._fused(theta, lp, grad)
         k = theta.shape[0]
         prev = torch.backends.cuda.matmul.allow_tf32
@@ -91,13 +97,13 @@ class LogisticRegressionEvaluator:
         k = theta.shape[0]
         need = -(-k // 128) * 128 * self.d
         if self.theta_b.numel() < need:
-            self.theta_b = torch.empty(need, dtype=torch.bfloat16, device="cuda")
+            self.theta_b = torch.empty(need, dtype=self.h16, device="cuda")
         g = grad if grad is not None else torch.empty((k, self.d), dtype=torch.float64, device="cuda")
         th = theta.contiguous()
-        st = _lib.lib().fsmc_logreg_tc_eval(th.data_ptr(), k, self.theta_b.data_ptr(),
-                                            self.Xb.data_ptr(), self.XTb.data_ptr(),
-                                            self.xty.data_ptr(), self.n_obs, self.d, lp.data_ptr(),
-                                            g.data_ptr(), _lib.stream_ptr())
+        st = _lib.lib().fsmc_logreg_tc_eval2(th.data_ptr(), k, self.theta_b.data_ptr(),
+                                             self.Xb.data_ptr(), self.XTb.data_ptr(),
+                                             self.xty.data_ptr(), self.n_obs, self.d, lp.data_ptr(),
+                                             g.data_ptr(), self.operand, _lib.stream_ptr())
         if st != 0:
             raise RuntimeError("fsmc_logreg_tc_eval: " +
                                _lib.lib().fsmc_logreg_tc_last_error().decode())

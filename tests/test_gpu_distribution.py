@@ -1,0 +1,77 @@
+"""Distributional parity where bit parity is not the contract (SURVEY.md 8c,
+c5 item 4; the reference pins posterior moments the same way,
+/root/reference/pkg/tests/test_acceptance.py:137-173): reduced-precision
+batched evaluators against the fp64 evaluator, two independent seeds each,
+compared chain mean by chain mean (tests/distribution_checks.py: Monte Carlo
+standard errors of the means, the spread, and two-sample KS, Bonferroni over
+the dimensions at family-wise level 0.01)."""
+
+import json
+import os
+
+import pytest
+
+from distribution_checks import assert_same_law, compare_runs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fm():
+    import paper_2503_17405_b200 as fm
+    return fm
+
+
+def _nuts_run(fm, X, y, precision, m, n, seed, eps):
+    from paper_2503_17405_b200.dense import LogisticRegressionEvaluator
+    bundle = fm.nuts_kernel(eps, 10)
+    target = fm.targets.logistic_regression_target(X, y)
+    ev = LogisticRegressionEvaluator(X, y, precision=precision)
+    s, _ = fm.run_fsm_batched(bundle, target, fm.init_batch(bundle, target, m, seed), n,
+                              step_variant="bundled", evaluator=ev, output="torch", surplus=False)
+    return s.cpu().numpy()
+
+
+_C5_REF = {}
+
+
+def _c5_reference(fm, X, y, m, n):
+    """The fp64-evaluator run, shared by the precisions compared against it."""
+    if (m, n) not in _C5_REF:
+        _C5_REF[(m, n)] = _nuts_run(fm, X, y, "fp64", m, n, 5, 0.01)
+    return _C5_REF[(m, n)]
+
+
+@pytest.mark.parametrize("precision", ["fp16-tc", "bf16-tc"])
+def test_c5_shape_reduced_precision_posterior_matches_fp64(fm, precision):
+    """BASELINE config 5's target (N = 100,000 observations, d = 256, the bench's
+    data and step size): NUTS driven by the fused tcgen05 evaluator samples the
+    same posterior as NUTS driven by the fp64 evaluator.  512 chains, 20
+    samples each, the first 8 dropped (the chains start at 0, the posterior
+    mean is |theta*| ~ 16 away)."""
+    import bench
+    cfg = bench.CONFIGS["c5"]
+    X, y = bench.logreg_data(cfg)
+    m, n, burn = 512, 20, 8
+    a = _c5_reference(fm, X, y, m, n)
+    b = _nuts_run(fm, X, y, precision, m, n, 6, 0.01)
+    r = compare_runs(a, b, burn)
+    out = os.environ.get("FSMC_REPORT_OUT")
+    if out:
+        with open(os.path.join(out, f"c5_distribution_{precision}.json"), "w") as f:
+            json.dump(r, f, indent=1)
+    print(f"\nC5 shape, {precision} vs fp64: max |mean diff| {r['max_mean_z']:.2f} s.e. "
+          f"(bound {r['z']:.2f}), spread {r['max_logvar_ratio_over_tol']:.2f} of its bound, "
+          f"min KS p {r['min_ks_p']:.3g}")
+    assert r["ok_mean"] and r["ok_var"] and r["ok_ks"], r
+
+
+def test_small_design_reduced_precision_posteriors_match_fp64(fm):
+    """A 2048-observation design (posterior ~7x wider than at C5): the fused
+    bf16 tcgen05 evaluator and the cuBLAS TF32 one against fp64."""
+    from paper_2503_17405_b200.targets import logistic_regression_data
+    X, y = logistic_regression_data(2048, 256, seed=1)
+    m, n, burn = 512, 30, 10
+    ref = _nuts_run(fm, X, y, "fp64", m, n, 5, 0.05)
+    for precision, seed in (("bf16-tc", 6), ("fp16-tc", 8), ("tf32", 7)):
+        assert_same_law(ref, _nuts_run(fm, X, y, precision, m, n, seed, 0.05), burn)
