@@ -381,7 +381,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
                     lanes: int = 0, evaluator=None, draw_window: int = 0,
                     prior_transform=None, draw_parts: int = 1, prior_parts: int = 1,
-                    _timing: dict | None = None):
+                    stop_sync=None, _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
@@ -407,6 +407,12 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     (bit-identical to the default mode); or a callable ``f(nu[k, d])``
     transforming the rows in place.  ``prior_parts`` (1..8) splits the chains
     in parts whose rounds overlap on their own streams.
+
+    ``stop_sync`` (a sharded batch, ``distributed.stop_sync(group)``): the
+    stop tick, completion and first failure are reduced over every rank's
+    shard, so ``tick_count``, the surplus ticks behind the aggregate
+    counters and the raised failure are the whole batch's (chain indices
+    global); ``distributed.global_ledger`` then merges the shard ledgers.
 
     ``draw_window`` (DRMH kernels): generate each chain's next ``draw_window``
     PRNG draws in a separate full-occupancy kernel and let the step kernel
@@ -495,19 +501,37 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     else:
         tick_count = limit
     first_err = int(info[errored, 3].min()) if bool(errored.any()) else _NO_LIMIT
+    g_err = None
+    if stop_sync is not None:
+        # sharded batch: the reference's stop rule is global (lockstep.py:359-366)
+        tick_count, all_done, g_key, g_rec = stop_sync(*_shard_stop(batch, info, key, tick_count,
+                                                                    all_done))
+        if not all_done:
+            tick_count = limit
+        first_err = g_key >> 24 if g_key < _NO_LIMIT else _NO_LIMIT
     run_to = min(tick_count, first_err)
     if run_to < _NO_LIMIT and (surplus or first_err < _NO_LIMIT) and int(cticks.min()) < run_to:
         launch(1, run_to)
         info, key = batch.host_summary()
     else:
         torch.cuda.synchronize()
+    if stop_sync is not None:
+        # the surplus ticks may have failed earlier than any failure seen so far
+        _, _, g_key, g_rec = stop_sync(*_shard_stop(batch, info, key, tick_count, all_done))
+        if g_key < _NO_LIMIT:
+            g_err = (g_key, g_rec)
     walltime = time.perf_counter() - t0
     if _timing is not None:
         _timing["run_kernel_ms"] = ev[0].elapsed_time(ev[1])
     batch.active_mask = [False] * m
     batch._ran = True
 
-    if key != (1 << 64) - 1:
+    if g_err is not None:
+        (g_key, (kind, label, eiter)) = g_err
+        if (g_key >> 24) <= tick_count:
+            raise KernelRunError(chain=g_key & ((1 << 24) - 1), iteration=eiter,
+                                 cause=_cause(bundle, kind, label))
+    elif stop_sync is None and key != (1 << 64) - 1:
         j = key & ((1 << 24) - 1)
         kind, etick_j, label, eiter = (int(v) for v in info[j, 2:6])
         if etick_j <= tick_count:
@@ -527,6 +551,17 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         host.copy_(samples, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return host.numpy(), ledger
+
+
+def _shard_stop(batch, info, key, tick_count, all_done):
+    """This shard's stop-rule fields for distributed.stop_sync: the chunked
+    stop tick, completion, and its first failure as a key over global chain
+    indices (tick << 24 | chain_offset + j) with (kind, label, sample index)."""
+    if key == (1 << 64) - 1:
+        return tick_count, all_done, _NO_LIMIT, (0, 0, 0)
+    j = key & ((1 << 24) - 1)
+    kind, etick, label, eiter = (int(v) for v in info[j, 2:6])
+    return tick_count, all_done, (etick << 24) | (batch.chain_offset + j), (kind, label, eiter)
 
 
 def _device_evaluator(target, family: int, lanes: int):

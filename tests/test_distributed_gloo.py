@@ -30,7 +30,14 @@ def local_moments(x, burn):
                 out[t] = (c[: n - lag] * c[lag:]).sum(axis=(0, 1)) / n
         return out
 
-    return LocalMoments(n, means, y.var(axis=0).max(axis=0), tile)
+    def every_lag():
+        """sum over this shard's chains of every lag's autocovariance (by FFT,
+        as diag_moments' acov_all does on the device)"""
+        size = 1 << int(np.ceil(np.log2(2 * n)))
+        f = np.fft.rfft(c, n=size, axis=0)
+        return np.fft.irfft((f * np.conj(f)).sum(axis=1), n=size, axis=0)[:n].real / n
+
+    return LocalMoments(n, means, y.var(axis=0).max(axis=0), tile, every_lag)
 
 
 def global_moments(x, burn):
@@ -50,18 +57,37 @@ def data():
     return x
 
 
-def worker(rank, world, port, q):
+def worker(rank, world, port, q, every_lag=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2503_17405_b200 import analysis, distributed
     x = data()
     lo, hi = distributed.shard_range(x.shape[1], rank, world)
-    mom = distributed.allreduce_moments(local_moments(x[:, lo:hi], 30))
-    ess = analysis.ess_from_moments(mom)
+    loc = local_moments(x[:, lo:hi], 30)
+    mom = distributed.allreduce_moments(loc)
+    if every_lag:   # the all-lags path (C3/C5: slowly mixing chains) instead of lag tiles
+        full = mom.acov_all() / mom.m
+        ess = analysis._geyer_all(full, mom)[0]
+        per = tuple(ess)
+    else:
+        per = analysis.ess_from_moments(mom).per_dimension
     rh = analysis.rhat_from_moments(mom)
     if rank == 0:
-        q.put((ess.per_dimension, tuple(rh)))
+        q.put((per, tuple(rh)))
     dist.destroy_process_group()
+
+
+def _spawn(target, world, *extra):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + extra) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    return [q.get(timeout=10) for _ in range(q.qsize() if hasattr(q, "qsize") else 1)]
 
 
 def free_port():
@@ -74,16 +100,7 @@ def free_port():
 
 def test_sharded_diagnostics_match_single_process():
     from paper_2503_17405_b200 import analysis
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    for p in procs:
-        p.join(120)
-        assert p.exitcode == 0
-    ess_dist, rh_dist = q.get(timeout=10)
+    (ess_dist, rh_dist), = _spawn(worker, 2)
     x = data()
     mom = global_moments(x, 30)
     ess = analysis.ess_from_moments(mom)
@@ -101,3 +118,64 @@ def test_shard_ranges_partition_the_chains():
         spans = [shard_range(m, r, w) for r in range(w)]
         assert spans[0][0] == 0 and spans[-1][1] == m
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_sharded_every_lag_path_matches_single_process():
+    """acov_all (one transform over every lag, the path C3/C5 take) all-reduced
+    over two ranks equals the single-process all-lags sums."""
+    from paper_2503_17405_b200 import analysis
+    (ess_dist, rh_dist), = _spawn(worker, 2, True)
+    x = data()
+    loc = local_moments(x, 30)
+    mom = global_moments(x, 30)
+    ess = analysis._geyer_all(loc.acov_all() / x.shape[1], mom)[0]
+    assert np.allclose(ess_dist, ess, rtol=1e-10)
+    from ess_reference import ess_numpy
+    for k in range(x.shape[2]):
+        assert ess[k] == pytest.approx(ess_numpy(x[30:, :, k].T), rel=1e-9)
+
+
+def _oracle_full():
+    from oracle import oracle as O
+    return O.run_fsm(O.drmh(30, 0.5), O.mog(10, 0.9, [-3.0, 0.0, 3.0]), 9, 40, 3,
+                     variant="bundled", nthreads=2)
+
+
+def ledger_worker(rank, world, port, q):
+    """Each rank holds its shard's columns of a real (oracle) ledger; the merged
+    ledger must be the full one.  Then the stop rule: the max stop tick, the
+    completion flag and the smallest failure key with its owner's record."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_17405_b200 import distributed
+    from paper_2503_17405_b200.lockstep import CostLedger
+    full = _oracle_full()
+    lo, hi = distributed.shard_range(9, rank, world)
+    blocks = np.array([rank + 1, 10 * (rank + 1), 100 * (rank + 1)], dtype=np.int64)
+    led = CostLedger(iter_counts=full["iter_counts"][:, lo:hi],
+                     loop_exec_counts={2: full["iter_counts"][:, lo:hi]},
+                     tick_count=500 + 100 * rank, block_exec_counts=blocks, charged_cost=0.0,
+                     walltime=1.0 + rank, regime="fsm-bundled", tick_cost=2.0,
+                     native_shared_evals=7 * (rank + 1), sample_ticks=full["sample_ticks"][:, lo:hi])
+    g = distributed.global_ledger(led)
+    sync = distributed.stop_sync()
+    big = 1 << 62
+    key = ((450 << 24) | 7) if rank == 1 else big
+    s1 = sync(500 + 100 * rank, True, key, (1, 2, 3) if rank == 1 else (0, 0, 0))
+    s2 = sync(300, rank == 0, big, (0, 0, 0))
+    q.put((rank, g.iter_counts, g.loop_exec_counts[2], g.sample_ticks, g.block_exec_counts.tolist(),
+           g.native_shared_evals, g.tick_count, g.walltime, g.charged_cost, s1, s2))
+    dist.destroy_process_group()
+
+
+def test_global_ledger_and_stop_rule_over_two_ranks():
+    outs = _spawn(ledger_worker, 2)
+    full = _oracle_full()
+    assert len(outs) == 2
+    for (rank, it, lx, st, blocks, shared, ticks, wall, charged, s1, s2) in outs:
+        assert np.array_equal(it, full["iter_counts"]) and np.array_equal(lx, full["iter_counts"])
+        assert np.array_equal(st, full["sample_ticks"])
+        assert blocks == [3, 30, 300] and shared == 21
+        assert ticks == 600 and wall == 2.0 and charged == 1200.0
+        assert s1 == (600, True, (450 << 24) | 7, (1, 2, 3))
+        assert s2[0] == 300 and s2[1] is False and s2[2] == 1 << 62

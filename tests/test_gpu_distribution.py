@@ -42,17 +42,26 @@ def _c5_reference(fm, X, y, m, n):
     return _C5_REF[(m, n)]
 
 
-@pytest.mark.parametrize("precision", ["fp16-tc", "bf16-tc"])
+# the bf16 operands fail at this size (theta rounded to 8 mantissa bits moves
+# a 1e5-term log density by several nats: measured max mean shift 9.4 s.e.,
+# KS p 2e-37, profiles/r04_c5_distribution.json); fp16 is the shipped one
+C5_DIST = {"m": 1024, "n": 60, "burn": 30}
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp16-tc",
+                                       pytest.param("bf16-tc", marks=pytest.mark.xfail(
+                                           strict=True, reason="bf16 theta biases the C5 posterior"))])
 def test_c5_shape_reduced_precision_posterior_matches_fp64(fm, precision):
     """BASELINE config 5's target (N = 100,000 observations, d = 256, the bench's
     data and step size): NUTS driven by the fused tcgen05 evaluator samples the
-    same posterior as NUTS driven by the fp64 evaluator.  512 chains, 20
-    samples each, the first 8 dropped (the chains start at 0, the posterior
-    mean is |theta*| ~ 16 away)."""
+    same posterior as NUTS driven by the fp64 evaluator.  1024 chains, 60
+    samples each, the first 30 dropped (the chains start at 0, the posterior
+    mean is |theta*| ~ 16 away).  "fp64" against itself (another seed) is the
+    harness's control at this horizon."""
     import bench
     cfg = bench.CONFIGS["c5"]
     X, y = bench.logreg_data(cfg)
-    m, n, burn = 512, 20, 8
+    m, n, burn = C5_DIST["m"], C5_DIST["n"], C5_DIST["burn"]
     a = _c5_reference(fm, X, y, m, n)
     b = _nuts_run(fm, X, y, precision, m, n, 6, 0.01)
     r = compare_runs(a, b, burn)
