@@ -7,7 +7,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -Xptxa
 CSRC := paper_2503_17405_b200/csrc
 BUILD ?= build
 LIB ?= paper_2503_17405_b200/libfsmc.so
-UNITS := fsmc fam_drmh fam_ess fam_nuts fam_slice logreg_tc gp_chol
+UNITS := fsmc fam_drmh fam_ess fam_nuts fam_slice logreg_tc gp_chol prior_trmm
 OBJS := $(addprefix $(BUILD)/,$(addsuffix .o,$(UNITS)))
 HDR := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/fsmc.h
 

@@ -52,7 +52,7 @@ CONFIGS = {
                family="nuts", m=16384, n=1000, d=100, variant="bundled", m_cpu=16),
     "c4": dict(workload="C4: elliptical slice FSM, GP-classification latent d=1024 (f-space)",
                family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4,
-               prior_transform="trmm", prior_parts=3),
+               prior_transform="dmma", prior_parts=3),
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; fp64 chain state, log density and gradient by the fused "
                         "tcgen05 kernel across chains (bf16 operands, fp32 accumulation)",
@@ -196,13 +196,14 @@ def main():
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--no-lockstep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end legs (A/B runs)")
     ap.add_argument("--draw-window", type=int, default=-1,
                     help="DRMH pre-drawn window in draws (0: inline generator; -1: config default)")
     ap.add_argument("--draw-parts", type=int, default=0,
                     help="DRMH windows: 1 or 2 chain halves overlapped on two streams (0: config)")
     ap.add_argument("--prior-parts", type=int, default=0,
                     help="ESS batched prior: chain parts overlapped on their own streams (0: config)")
-    ap.add_argument("--prior", default="", choices=["", "none", "trmm", "gemm", "device"],
+    ap.add_argument("--prior", default="", choices=["", "none", "dmma", "trmm", "gemm", "device"],
                     help="ESS dense prior: batched nu = L eps per round (default: config's)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -357,13 +358,18 @@ def main():
                                   prior_parts=cfg.get("prior_parts", 1))
 
     e2e_s, led_h = [], None
-    for s in range(3):           # the first call also pins the host buffers (cached after)
+    for s in range(0 if args.no_e2e else 3):   # the first call also pins the host buffers
         smp = led_h = None
         barrier()
         t0 = time.perf_counter()
         smp, led_h = e2e_run(s, "numpy")
         barrier()
         e2e_s.append(time.perf_counter() - t0)
+    if args.no_e2e:
+        e2e_s = [float("nan")] * 2
+        smp = np.zeros(0)
+        led_h = type("L", (), {"loop_exec_counts": {}, "iter_counts": np.zeros(0),
+                               "block_exec_counts": np.zeros(0)})()
     t_e2e = max_over_ranks(min(e2e_s[1:]))
     d2h = smp.nbytes + sum(a.nbytes for a in led_h.loop_exec_counts.values()) + \
         led_h.iter_counts.nbytes + np.asarray(led_h.block_exec_counts).nbytes + 8 * (7 * m + 1)
@@ -376,8 +382,8 @@ def main():
            "ms": [round(1e3 * v, 3) for v in e2e_s]}
     del smp, led_h
     # the same with the samples left in HBM (output="torch"), plus the device ESS
-    e2e_dev = []
-    for s in range(2):
+    e2e_dev = [float("nan")] if args.no_e2e else []
+    for s in range(0 if args.no_e2e else 2):
         barrier()
         t0 = time.perf_counter()
         smp, _ = e2e_run(10 + s, "torch")

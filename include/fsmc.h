@@ -317,6 +317,16 @@ fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, 
  * prior transform for fsmc_advance_prior. */
 fsmc_status fsmc_prior_apply(const fsmc_target* t, double* nu, int64_t k, void* stream_);
 
+/* nu[r] = L nu[r] for the k parked rows of a round (the ESS prior transform,
+ * elliptical.py:73) on the fp64 tensor cores: a hand-written DMMA
+ * (mma.sync m8n8k4 f64) triangular product out = eps L^T over 128 x 128
+ * tiles, k slabs only up to each tile's diagonal; tmp [k][dim] is scratch.
+ * Not bit-identical to the per-chain summation (tensor-core accumulation
+ * order); the sampler's step counts match the reference's (tested). dim
+ * must be even. */
+fsmc_status fsmc_prior_trmm(const fsmc_target* t, double* nu, double* tmp, int64_t k, void* stream);
+const char* fsmc_prior_trmm_last_error(void);
+
 /* Logistic-regression evaluation epilogue over a tile of chains: given
  * Z [rows][N] = Theta X^T (fp32, from the contraction), labels y [N]:
  *   lp[r]   += sum_i y_i z_ri - log(1 + e^{z_ri})     (fp64 accumulation)

@@ -134,6 +134,9 @@ def lib():
         [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _P]
     L.fsmc_prior_apply.restype = S
     L.fsmc_prior_apply.argtypes = [ctypes.POINTER(Target), _P, ctypes.c_int64, _P]
+    L.fsmc_prior_trmm.restype = S
+    L.fsmc_prior_trmm.argtypes = [ctypes.POINTER(Target), _P, _P, ctypes.c_int64, _P]
+    L.fsmc_prior_trmm_last_error.restype = ctypes.c_char_p
     L.fsmc_lockstep_run.restype = S
     L.fsmc_lockstep_run.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                     ctypes.POINTER(State), ctypes.c_int64,

@@ -66,13 +66,84 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
   }
 }
 
+// The same window fill with U slots per lane per pass: the U raw draws, their
+// classification and their central-branch polynomials are straight-line code
+// (the branch-free division), so U independent dependency chains interleave;
+// the tail queue is then fed once per pass.  Bit-identical to the kernel above.
+#ifndef FSMC_GEN_U
+#define FSMC_GEN_U 4
+#endif
+template <int U>
+__global__ void __launch_bounds__(256) drmh_draws_ilp_kernel(Params p) {
+  __shared__ double qy_all[8][kDrawChunk];
+  __shared__ unsigned qk_all[8][kDrawChunk];
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = (int)p.window, d = p.t.dim, per = d + 1;
+  double* qy = qy_all[wid];
+  unsigned* qk = qk_all[wid];
+  const unsigned lt = (1u << lane) - 1u;
+  const int step = 32 % per;             // phase advance between a lane's slots
+  const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
+  for (long long j = p.j_lo + (long long)blockIdx.x * nw + wid; j < p.j_hi; j += (long long)gridDim.x * nw) {
+    const int64_t* q = p.st.ints + (size_t)j * FSMC_NINT;
+    if (q[FSMC_I_ERR_KIND] != FSMC_E_NONE || q[FSMC_I_COUNT] >= n_stop || q[FSMC_I_TICK] >= p.tick_limit)
+      continue;
+    const uint64_t ctr0 = (uint64_t)q[FSMC_I_COUNTER];
+    const uint64_t hsc = hash_seed_stream(p.st.seed, (uint64_t)q[FSMC_I_STREAM]);
+    int phase = (int)((ctr0 - (uint64_t)q[FSMC_I_DRAW0]) % (uint64_t)per) + lane % per;
+    if (phase >= per) phase -= per;
+    double* out = p.draws + (size_t)j * W;
+    for (int c0 = 0; c0 < W; c0 += kDrawChunk) {
+      const int c1 = min(W, c0 + kDrawChunk);
+      int nt = 0;
+      for (int k0 = c0; k0 < c1; k0 += 32 * U) {
+        double bd[U], yr[U], vc[U];
+        bool neg[U], cen[U], uni[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {   // prng.py:58-81, 103-111
+          bd[u] = (double)(bits(hsc, ctr0 + (uint64_t)(k0 + 32 * u + lane)) >> 11);
+          uni[u] = phase == d;
+          phase += step;
+          phase = phase >= per ? phase - per : phase;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) cen[u] = ndtri_classify((bd[u] + 0.5) * INV_2_53, &yr[u], &neg[u]);
+#pragma unroll
+        for (int u = 0; u < U; u++) vc[u] = ndtri_central_sl(yr[u]);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int k = k0 + 32 * u + lane;
+          const bool live = k < c1;
+          const double v = uni[u] ? bd[u] * INV_2_53 : vc[u];     // prng.py:97-100
+          const bool tail = live && !uni[u] && !cen[u];
+          if (live && !tail) out[k] = v;
+          const unsigned bt = __ballot_sync(0xffffffffu, tail);
+          if (tail) {
+            const int pos = nt + __popc(bt & lt);
+            qy[pos] = yr[u];
+            qk[pos] = (unsigned)k | (neg[u] ? 0x80000000u : 0u);
+          }
+          nt += __popc(bt);
+        }
+      }
+      __syncwarp();
+      for (int t = lane; t < nt; t += 32) {
+        const unsigned kk = qk[t];
+        out[kk & 0x7fffffffu] = ndtri_tail(qy[t], (kk >> 31) != 0);
+      }
+      __syncwarp();
+    }
+  }
+}
+
 static cudaError_t launch_drmh_draws(const Params& p, int num_sms, cudaStream_t s) {
   const int threads = 256, nw = threads / 32;
   long long need = (p.j_hi - p.j_lo + nw - 1) / nw;
   const int per_sm = p.draw_blocks_per_sm > 0 ? p.draw_blocks_per_sm : 8;
   int blocks = (int)std::max<long long>(1, std::min<long long>(need, (long long)num_sms * per_sm));
   count_launch();
-  drmh_draws_kernel<<<blocks, threads, 0, s>>>(p);
+  if (FSMC_GEN_U > 1) drmh_draws_ilp_kernel<FSMC_GEN_U><<<blocks, threads, 0, s>>>(p);
+  else drmh_draws_kernel<<<blocks, threads, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -137,13 +137,18 @@ def _cublas():
 class PriorTransform:
     """nu[r] = L nu[r] for the rows of a round, L lower-triangular (the
     target's prior factor; ``Lt`` = Lᵀ row-major = L column-major).
-    ``method="trmm"``: cuBLAS DTRMM (half the flops of a dense product);
-    ``"gemm"``: a dense DGEMM ``rows @ Lᵀ``."""
+    ``method="dmma"``: the hand-written fp64 tensor-core triangular product
+    (``fsmc_prior_trmm``, csrc/prior_trmm.cu); ``"trmm"``: cuBLAS DTRMM
+    (half the flops of a dense product); ``"gemm"``: a dense DGEMM
+    ``rows @ Lᵀ``."""
 
-    def __init__(self, Lt: torch.Tensor, method: str = "trmm"):
-        if method not in ("trmm", "gemm"):
-            raise ValueError("method must be trmm or gemm")
+    def __init__(self, Lt: torch.Tensor, method: str = "dmma", target=None):
+        if method not in ("dmma", "trmm", "gemm"):
+            raise ValueError("method must be dmma, trmm or gemm")
+        if method == "dmma" and target is None:
+            raise ValueError("the dmma transform needs the target (its device descriptor)")
         self.Lt, self.method, self.d = Lt, method, Lt.shape[0]
+        self.tgt = target.struct() if target is not None else None
         self.tmp = None
         self.one = None
 
@@ -152,6 +157,14 @@ class PriorTransform:
         if self.tmp is None or self.tmp.shape[0] < k:
             self.tmp = torch.empty_like(rows)
         out = self.tmp[:k]
+        if self.method == "dmma":
+            import ctypes
+            st = _lib.lib().fsmc_prior_trmm(ctypes.byref(self.tgt), rows.data_ptr(), out.data_ptr(),
+                                            k, _lib.stream_ptr())
+            if st != 0:
+                raise _lib.EngineError("fsmc_prior_trmm: " +
+                                       _lib.lib().fsmc_prior_trmm_last_error().decode())
+            return
         if self.method == "gemm":
             torch.mm(rows, self.Lt, out=out)
         else:

@@ -400,9 +400,10 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     ``prior_transform`` (elliptical kernel with a dense Gaussian prior):
     batch the INIT block's nu = L eps across chains (``fsmc_advance_prior``).
     Chains run with the plugin evaluated in place until their next INIT,
-    park eps, and all parked rows are transformed in one call.  "gemm": one
-    fp64 GEMM ``eps @ L^T`` (cuBLAS DGEMM; values within its rounding);
-    "trmm": the same product as a triangular cuBLAS DTRMM (half the flops);
+    park eps, and all parked rows are transformed in one call.  "dmma": the
+    hand-written fp64 tensor-core triangular product (``fsmc_prior_trmm``;
+    values within its rounding); "gemm": one fp64 GEMM ``eps @ L^T`` (cuBLAS
+    DGEMM); "trmm": the same product as a triangular cuBLAS DTRMM;
     "device": ``fsmc_prior_apply``, the sampling kernel's summation order
     (bit-identical to the default mode); or a callable ``f(nu[k, d])``
     transforming the rows in place.  ``prior_parts`` (1..8) splits the chains
@@ -627,9 +628,9 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
     req_count = torch.zeros(parts, dtype=torch.int32, device="cuda")
     lib = _lib.lib()
     kern, tgt = batch.kernel, target.struct()
-    if transform in ("gemm", "trmm"):
+    if transform in ("gemm", "trmm", "dmma"):
         from .dense import PriorTransform
-        transform = [PriorTransform(target.device_arrays()["prior_t"], transform)
+        transform = [PriorTransform(target.device_arrays()["prior_t"], transform, target)
                      for _ in range(parts)]
         for h, t in enumerate(transform):    # scratch allocated up front, on this stream
             t.tmp = torch.empty((bounds[h][1] - bounds[h][0], d), dtype=torch.float64, device="cuda")
@@ -638,7 +639,7 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
             _lib.check(lib.fsmc_prior_apply(ctypes.byref(tgt), rows.data_ptr(), rows.shape[0],
                                             _lib.stream_ptr()), "fsmc_prior_apply")
     elif not callable(transform):
-        raise ValueError("prior_transform must be 'trmm', 'gemm', 'device' or a callable")
+        raise ValueError("prior_transform must be 'dmma', 'trmm', 'gemm', 'device' or a callable")
     if not isinstance(transform, list):
         transform = [transform] * parts
     stats = {"rounds": 0, "prior_transforms": 0}

@@ -56,36 +56,53 @@ def _run(fm, name, lo, hi, stop_sync=None):
 
 def worker(rank, world, port, name, q):
     import sys
-    sys.path.insert(0, ROOT)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    import torch.distributed as dist
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    import paper_2503_17405_b200 as fm
-    from paper_2503_17405_b200 import distributed
-    m = _case(name, fm)[2]
-    lo, hi = distributed.shard_range(m, rank, world)
-    out = _run(fm, name, lo, hi, distributed.stop_sync())
-    if out[0] == "error":
-        q.put((rank, out))
-    else:
-        s, led = out
-        g = distributed.global_ledger(led)
-        q.put((rank, (lo, hi, s, g.iter_counts, g.sample_ticks, g.tick_count,
-                      np.asarray(g.block_exec_counts).tolist(), g.native_shared_evals,
-                      led.tick_count)))
-    dist.destroy_process_group()
+    import traceback
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2503_17405_b200 as fm
+        from paper_2503_17405_b200 import distributed
+        m = _case(name, fm)[2]
+        lo, hi = distributed.shard_range(m, rank, world)
+        out = _run(fm, name, lo, hi, distributed.stop_sync())
+        if out[0] == "error":
+            q.put((rank, out))
+        else:
+            s, led = out
+            g = distributed.global_ledger(led)
+            q.put((rank, (lo, hi, s, g.iter_counts, g.sample_ticks, g.tick_count,
+                          np.asarray(g.block_exec_counts).tolist(), g.native_shared_evals,
+                          led.tick_count)))
+        dist.destroy_process_group()
+    except BaseException:
+        q.put((rank, ("exception", traceback.format_exc())))
 
 
 def _spawn(name, world=2):
+    import queue
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=worker, args=(r, world, port, name, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=600) for _ in range(world))
+    res = {}
+    try:
+        for _ in range(world):
+            rank, out = q.get(timeout=240)
+            res[rank] = out
+            if out[0] == "exception":     # the other rank may now wait in a collective
+                raise AssertionError(f"rank {rank} failed:\n{out[1]}")
+    except queue.Empty:
+        raise AssertionError(f"ranks {sorted(set(range(world)) - set(res))} sent nothing in 240 s")
+    finally:
+        for p in procs:
+            p.join(60)
+            if p.is_alive():
+                p.kill()
     for p in procs:
-        p.join(120)
         assert p.exitcode == 0
     return res
 
