@@ -53,17 +53,30 @@ CONFIGS = {
     "c4": dict(workload="C4: elliptical slice FSM, GP-classification latent d=1024 (f-space)",
                family="ess", m=8192, n=200, d=1024, variant="amortized", m_cpu=4,
                prior_transform="dmma", prior_parts=3),
+    # the fp32 throughput mode on configs 2 and 3 (separate lines, never the headline)
+    "c2f": dict(workload="C2 in the fp32 throughput mode: DRMH FSM, correlated MoG d=10 (rho=0.9, "
+                         "modes -3/0/3), M=100, scale=0.1, bundled; fp32 state and arithmetic, "
+                         "fp64 reference draws rounded once; distributional parity only",
+                family="drmh", m=65536, n=1000, d=10, variant="bundled", m_cpu=256,
+                draw_window=4070, draw_parts=4, precision="fp32"),
+    "c3f": dict(workload="C3 in the fp32 throughput mode: NUTS FSM, equicorrelated Gaussian d=100 "
+                         "rho=0.99, eps=0.05, depth 10; fp32 state and arithmetic; distributional "
+                         "parity only",
+                family="nuts", m=16384, n=1000, d=100, variant="bundled", m_cpu=16,
+                precision="fp32"),
     "c5": dict(workload="C5: NUTS FSM, Bayesian logistic regression N=100k d=256, eps=0.01, "
                         "depth 10; fp64 chain state, log density and gradient by the fused "
-                        "tcgen05 kernel across chains (bf16 operands, fp32 accumulation)",
+                        "tcgen05 kernel across chains (fp16 operands, fp32 accumulation; "
+                        "distributional parity: profiles/r04_c5_distribution.json)",
                family="nuts", m=131072, n=32, d=256, variant="bundled", m_cpu=16, n_cpu=2, n_obs=100_000,
-               batched="bf16-tc"),
+               batched="fp16-tc"),
 }
 
 
 # arithmetic of the line: fp64 everywhere unless a reduced-precision batched
 # evaluator computes the log density and gradient
 EVAL_DTYPE = {"bf16-tc": "f64 state / bf16 evaluator (fp32 accumulate)",
+              "fp16-tc": "f64 state / fp16 evaluator (fp32 accumulate)",
               "tf32-tc": "f64 state / tf32 evaluator (fp32 accumulate)",
               "tf32": "f64 state / tf32 evaluator (cuBLAS)"}
 
@@ -268,7 +281,8 @@ def main():
                                   evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
                                   prior_transform=cfg.get("prior_transform"),
                                   draw_parts=cfg.get("draw_parts", 1),
-                                  prior_parts=cfg.get("prior_parts", 1), _timing=timing)
+                                  prior_parts=cfg.get("prior_parts", 1),
+                                  precision=cfg.get("precision", "fp64"), _timing=timing)
 
     held = None
     for s in range(args.warmup):
@@ -355,7 +369,8 @@ def main():
                                   evaluator=evaluator, draw_window=cfg.get("draw_window", 0),
                                   prior_transform=cfg.get("prior_transform"),
                                   draw_parts=cfg.get("draw_parts", 1),
-                                  prior_parts=cfg.get("prior_parts", 1))
+                                  prior_parts=cfg.get("prior_parts", 1),
+                                  precision=cfg.get("precision", "fp64"))
 
     e2e_s, led_h = [], None
     for s in range(0 if args.no_e2e else 3):   # the first call also pins the host buffers
@@ -491,7 +506,7 @@ def main():
         # dominant work: the two contractions per evaluation, 4 N d flops each
         flops = 4.0 * cfg["n_obs"] * d * evals
         ach = flops / (kms / 1e3) / 1e12
-        bf16 = cfg["batched"] == "bf16-tc"
+        bf16 = cfg["batched"] in ("bf16-tc", "fp16-tc")      # same dense rate for fp16
         pk = peaks.get("bf16_tflops_sustained", 1395.2) * (1.0 if bf16 else 0.5)
         roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                 "frac": ach / pk, "traffic": None,
@@ -499,7 +514,8 @@ def main():
                            if bf16 else "cuBLAS TF32 GEMMs + fsmc_logreg_epilogue") +
                           " + fsm_advance_kernel<Nuts,128,2>",
                 "kernel_ms": kms, "algorithmic_flops": flops,
-                "note": "peak = measured sustained dense bf16 (half of it for TF32); whole run "
+                "note": "peak = measured sustained dense bf16 (fp16 has the same dense rate; half of "
+                        "it for TF32); whole run "
                         "(advance rounds + evaluations) timed"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -509,7 +525,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": EVAL_DTYPE.get(cfg.get("batched"), "f64"), "data": "synthetic",
+                "dtype": ("f32 (fp64 draws)" if cfg.get("precision") == "fp32" else
+                          EVAL_DTYPE.get(cfg.get("batched"), "f64")), "data": "synthetic",
                 "config": {"workload": cfg["workload"], "chains_per_gpu": m, "chains_total": m * world,
                            "n": n, "d": d, "variant": cfg["variant"],
                            "parallelism": f"chains sharded over {world} GPU(s), no data-path "

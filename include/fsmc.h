@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define FSMC_ABI_VERSION 4
+#define FSMC_ABI_VERSION 5
 #define FSMC_WORK_WORDS 256 /* uint32 words of fsmc_state.work */
 #define FSMC_NINT 32        /* int64 slots per chain in fsmc_state.ints */
 #define FSMC_MAX_MODES 8    /* mixture components in FSMC_T_MOG */
@@ -70,7 +70,13 @@ typedef struct fsmc_kernel {
   double divergence_threshold;  /* nuts */
   double slice_width;           /* slice: initial bracket width w */
   int32_t max_expansions;       /* slice: stepping-out budget */
-  int32_t pad;
+  int32_t precision;            /* 0: fp64 arithmetic, the parity path (default); 1: the fp32
+                                   throughput mode -- chain state and arithmetic in fp32, the
+                                   draws still the reference's fp64 values (each rounded once),
+                                   distributional parity only.  Compiled for the benchmark
+                                   targets (DRMH on the MoG / funnel, d <= 10; NUTS on the
+                                   equicorrelated Gaussian, d <= 128) in fsmc_run and the
+                                   windowed DRMH runs; FSMC_ERR_UNSUPPORTED elsewhere. */
 } fsmc_kernel;
 
 typedef struct fsmc_target {

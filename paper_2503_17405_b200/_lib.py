@@ -15,7 +15,7 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FSMC_LIB", os.path.join(HERE, "libfsmc.so"))
 
-ABI_VERSION = 4    # fsmc.h FSMC_ABI_VERSION
+ABI_VERSION = 5    # fsmc.h FSMC_ABI_VERSION
 WORK_WORDS = 256   # fsmc.h FSMC_WORK_WORDS
 FSMC_NINT = 32
 MAX_MODES = 8
@@ -50,7 +50,7 @@ class Kernel(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int32), ("max_tries", ctypes.c_int32),
                 ("proposal_scale", _D), ("step_size", _D), ("max_depth", ctypes.c_int32),
                 ("split_body", ctypes.c_int32), ("divergence_threshold", _D),
-                ("slice_width", _D), ("max_expansions", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("slice_width", _D), ("max_expansions", ctypes.c_int32), ("precision", ctypes.c_int32)]
 
 
 class Target(ctypes.Structure):

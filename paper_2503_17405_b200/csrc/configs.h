@@ -20,3 +20,7 @@
 // uses, so the batched device evaluator reduces in the run kernel's order
 #define FSMC_EVAL_CONFIGS(X) X(1, 1) X(1, 2) X(1, 4) X(1, 10) X(1, 16) X(2, 2) X(2, 5) X(4, 3) \
   X(4, 4) X(8, 2) X(32, 1) X(32, 2) X(32, 4) X(32, 8) X(128, 1) X(128, 2) X(128, 8)
+
+// fp32 throughput mode (fsmc_kernel.precision = 1): the benchmark configs only
+#define FSMC_DRMH_F32(X) X(1, 10, FSMC_T_MOG) X(1, 10, FSMC_T_FUNNEL)
+#define FSMC_NUTS_F32(X) X(32, 4, FSMC_T_GAUSS_EQUICORR)

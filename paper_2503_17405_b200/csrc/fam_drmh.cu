@@ -151,6 +151,16 @@ cudaError_t dispatch_drmh(int op, int g, int e, Params& p, const LaunchCtx& lc, 
                            uint64_t ps, long long off, const double* x0, double jit) {
   const int kind = p.t.kind;
   if (op == 6) return launch_drmh_draws(p, lc.num_sms, s);
+  if (p.k.precision == 1 && !p.k.split_body) {   // fp32 throughput mode: the sampling runs only
+#define F(GG, EE, TK)                                                                \
+  if (g == GG && e == EE && kind == TK) {                                            \
+    if (op == 5) return Launch<DrmhWF, GG, EE, TK>::window(p, lc, s);                \
+    if (op == 1) return Launch<DrmhF, GG, EE, TK>::run(p, lc, s);                    \
+  }
+    FSMC_DRMH_F32(F)
+#undef F
+    if (op == 1 || op == 5) return cudaErrorNotSupported;
+  }
   if (op == 5) {  // windowed run: the DR = true families
     if (p.k.split_body) {
 #define X(GG, EE) \

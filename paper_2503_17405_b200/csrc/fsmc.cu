@@ -337,6 +337,26 @@ fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_st
                               "n <= 56 and scratch 2n^2+2n+4 (scratch 0: batched evaluator only)");
   if (t->kind == FSMC_T_MOG && (t->n_modes < 1 || t->n_modes > FSMC_MAX_MODES))
     return fail(FSMC_ERR_ARG, "n_modes out of range");
+  if (k->precision != 0 && k->precision != 1) return fail(FSMC_ERR_ARG, "precision must be 0 (fp64) or 1 (fp32)");
+  return FSMC_OK;
+}
+
+// the fp32 throughput mode's compiled (family, lanes, elements, plugin) set
+bool f32_compiled(const fsmc_kernel* k, const fsmc_target* t, const GE& ge) {
+  bool ok = false;
+#define D(GG, EE, TK) ok = ok || (k->family == FSMC_DRMH && !k->split_body && ge.g == GG && ge.e == EE && t->kind == TK);
+  FSMC_DRMH_F32(D)
+#undef D
+#define N(GG, EE, TK) ok = ok || (k->family == FSMC_NUTS && ge.g == GG && ge.e == EE && t->kind == TK);
+  FSMC_NUTS_F32(N)
+#undef N
+  return ok;
+}
+fsmc_status check_f32(const fsmc_kernel* k, const fsmc_target* t, const GE& ge) {
+  if (k->precision == 1 && !f32_compiled(k, t, ge))
+    return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode is compiled for DRMH on the MoG / funnel "
+                                      "(d <= 10, one lane per chain) and NUTS on the equicorrelated "
+                                      "Gaussian (d <= 128, a warp per chain)");
   return FSMC_OK;
 }
 
@@ -435,6 +455,7 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
   GE ge;
   if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
     return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  if ((s = check_f32(k, t, ge)) != FSMC_OK) return s;
   Params p;
   memset(&p, 0, sizeof(p));
   p.k = *k; p.t = *t; p.st = *st;
@@ -514,6 +535,7 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
                          int32_t* req_chain, int32_t* req_count, int32_t lanes, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
+  if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
   if (!theta || !req_chain || !req_count || !lp || (k->family == FSMC_NUTS && !grad))
     return fail(FSMC_ERR_ARG, "advance needs theta, req_chain, req_count, lp (and grad for NUTS)");
   return advance_common(3, k, t, st, n, variant, order, tick_limit, mode, out, lp, grad, theta,
@@ -526,6 +548,7 @@ fsmc_status fsmc_advance_lockstep(const fsmc_kernel* k, const fsmc_target* t, fs
                                   int32_t lanes, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
+  if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
   if (!theta || !req_chain || !req_count || !lp || !level || (k->family == FSMC_NUTS && !grad))
     return fail(FSMC_ERR_ARG, "advance_lockstep needs theta, req_chain, req_count, lp, level (and grad for NUTS)");
   return advance_common(3, k, t, st, n, FSMC_PLAIN, nullptr, INT64_MAX, 0, out, lp, grad, theta,
@@ -538,6 +561,7 @@ fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_
                                int32_t* req_count, int32_t lanes, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
+  if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
   if (k->family != FSMC_ESS || t->prior_kind != FSMC_PRIOR_DENSE)
     return fail(FSMC_ERR_UNSUPPORTED, "the batched prior transform is for the elliptical kernel with a dense prior");
   if (!nu || !req_chain || !req_count)
@@ -553,6 +577,7 @@ fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, 
                                     int32_t part, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
+  if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
   if (k->family != FSMC_ESS || t->prior_kind != FSMC_PRIOR_DENSE)
     return fail(FSMC_ERR_UNSUPPORTED, "the batched prior transform is for the elliptical kernel with a dense prior");
   if (!nu || !req_chain || !req_count || part < 0)
@@ -620,6 +645,7 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   GE ge;
   if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
     return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
+  if ((s = check_f32(k, t, ge)) != FSMC_OK) return s;
   Params p;
   memset(&p, 0, sizeof(p));
   p.k = *k; p.t = *t; p.st = *st;
@@ -741,6 +767,7 @@ fsmc_status fsmc_profile_blocks(const fsmc_kernel* k, const fsmc_target* t, fsmc
                                 int64_t tick_limit, unsigned long long* cycles, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
+  if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
   if (!cycles || tick_limit < 0) return fail(FSMC_ERR_ARG, "profile needs cycles[16] and tick_limit >= 0");
   // one chain per warp where compiled: a lane group then never waits on
   // other chains' divergent blocks, so its clock deltas are its own blocks
@@ -767,6 +794,7 @@ fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
                               const fsmc_outputs* out, int32_t lanes, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
+  if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
   GE ge;
   if (!pick_config(k->family, t->dim, lanes, ge, t->kind))
     return fail(FSMC_ERR_UNSUPPORTED, "no compiled (lanes, elements) configuration for this dimension");
@@ -790,6 +818,7 @@ fsmc_status fsmc_lockstep_barrier_probe(const fsmc_kernel* k, const fsmc_target*
                                         int64_t iters, int32_t lanes, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
+  if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
   if (iters < 1) return fail(FSMC_ERR_ARG, "iters must be >= 1");
   GE ge;
   if (!pick_config(k->family, t->dim, lanes, ge, t->kind))

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
+#include <utility>
 
 #include "configs.h"
 #include "fsm_device.cuh"
@@ -52,8 +54,23 @@ template <int G>
 __host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : (G == 32 ? FSMC_WARP_MIN_BLOCKS : (G == 128 ? 4 : 1)); }
 // block-per-chain NUTS (G = 128, C5's advance kernel) keeps its registers: 4
 // resident blocks would spill its twelve-vector state
+// fp32 throughput-mode families (half the register footprint per vector):
+// more resident blocks
+#ifndef FSMC_F32_MIN_BLOCKS
+#define FSMC_F32_MIN_BLOCKS 5          // thread-per-chain groups
+#endif
+#ifndef FSMC_F32_WARP_MIN_BLOCKS
+#define FSMC_F32_WARP_MIN_BLOCKS 4     // warp-per-chain groups (NUTS: 12 vectors + checkpoints)
+#endif
+template <class FF>
+constexpr bool is_f32_family() {
+  return std::is_same<typename std::remove_reference<decltype(std::declval<FF&>().x[0])>::type, float>::value;
+}
 template <template <int, int> class F, int G, int E>
-__host__ __device__ constexpr int min_blocks_for() { return (G == 128 && F<G, E>::GRAD) ? 1 : min_blocks<G>(); }
+__host__ __device__ constexpr int min_blocks_for() {
+  return is_f32_family<F<G, E>>() ? (G == 1 ? FSMC_F32_MIN_BLOCKS : FSMC_F32_WARP_MIN_BLOCKS)
+                                  : ((G == 128 && F<G, E>::GRAD) ? 1 : min_blocks<G>());
+}
 
 struct LaunchCtx {
   int num_sms;
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run
 // draws at counters dbase .. dbase + window - 1 are in p.draws[j]; it ticks
 // while a tick's worst case (dim + 1 draws for DRMH) still fits.
 template <template <int, int> class F, int G, int E, int TK, int VAR = 0>
-__global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_window_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_window_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
   // no cooperative-normal scratch: the draws are pre-generated, and the

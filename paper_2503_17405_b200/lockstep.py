@@ -381,7 +381,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                     tick_chunk: int = TICK_CHUNK, *, surplus: bool = True, output: str = "numpy",
                     lanes: int = 0, evaluator=None, draw_window: int = 0,
                     prior_transform=None, draw_parts: int = 1, prior_parts: int = 1,
-                    stop_sync=None, _timing: dict | None = None):
+                    stop_sync=None, precision: str = "fp64", _timing: dict | None = None):
     """Run every chain's machine until each holds n samples (lockstep.py:308-416).
 
     ``surplus=False`` skips the reference's surplus ticks (steps of chains
@@ -408,6 +408,12 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     (bit-identical to the default mode); or a callable ``f(nu[k, d])``
     transforming the rows in place.  ``prior_parts`` (1..8) splits the chains
     in parts whose rounds overlap on their own streams.
+
+    ``precision="fp32"``: the throughput mode -- chain state and arithmetic
+    in fp32 (the draws are still the reference's fp64 values, each rounded
+    once; the HBM state and the samples stay float64).  Distributional
+    parity only (tests/test_gpu_distribution.py); compiled for DRMH on the
+    MoG / funnel (d <= 10) and NUTS on the equicorrelated Gaussian.
 
     ``stop_sync`` (a sharded batch, ``distributed.stop_sync(group)``): the
     stop tick, completion and first failure are reduced over every rank's
@@ -444,7 +450,14 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     egressed = False
     limit = (tick_budget // tick_chunk) * tick_chunk if tick_budget is not None else _NO_LIMIT
     lib = _lib.lib()
+    if precision not in ("fp64", "fp32"):
+        raise ValueError("precision must be 'fp64' or 'fp32'")
     kern, tgt = batch.kernel, target.struct()
+    if precision == "fp32":
+        if evaluator is not None or prior_transform is not None:
+            raise ValueError("the fp32 throughput mode runs the per-chain plugins only")
+        kern = _lib.Kernel.from_buffer_copy(batch.kernel)
+        kern.precision = 1
     ordv = (ctypes.c_int32 * K)(*order)
     variant = _VARIANT_ID[step_variant]
 

@@ -84,3 +84,35 @@ def test_small_design_reduced_precision_posteriors_match_fp64(fm):
     ref = _nuts_run(fm, X, y, "fp64", m, n, 5, 0.05)
     for precision, seed in (("bf16-tc", 6), ("fp16-tc", 8), ("tf32", 7)):
         assert_same_law(ref, _nuts_run(fm, X, y, precision, m, n, seed, 0.05), burn)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fp32_throughput_mode_matches_fp64_in_distribution(fm, name):
+    """The fp32 throughput mode (run_fsm_batched(precision="fp32"): chain state
+    and arithmetic in fp32, the reference's fp64 draws rounded once) against
+    the fp64 parity path on BASELINE configs 2 and 3's targets and kernels,
+    independent seeds, chain means compared as above."""
+    import bench
+    cfg = bench.CONFIGS[name]
+    bundle, target = bench.make_workload(cfg, fm)
+    m, n, burn = (4096, 400, 100) if name == "c2" else (2048, 200, 50)
+    runs = []
+    for prec, seed in (("fp64", 21), ("fp32", 22)):
+        s, _ = fm.run_fsm_batched(bundle, target, fm.init_batch(bundle, target, m, seed), n,
+                                  step_variant=cfg["variant"], output="torch", surplus=False,
+                                  precision=prec)
+        runs.append(s.cpu().numpy())
+    r = compare_runs(runs[0], runs[1], burn)
+    out = os.environ.get("FSMC_REPORT_OUT")
+    if out:
+        with open(os.path.join(out, f"fp32_distribution_{name}.json"), "w") as f:
+            json.dump(r, f, indent=1)
+    print(f"\n{name} fp32 vs fp64: max |mean diff| {r['max_mean_z']:.2f} s.e. (bound {r['z']:.2f}), "
+          f"spread {r['max_logvar_ratio_over_tol']:.2f} of its bound, min KS p {r['min_ks_p']:.3g}")
+    assert r["ok_mean"] and r["ok_var"] and r["ok_ks"], r
+
+
+def test_fp32_mode_rejects_uncompiled_configurations(fm):
+    bundle, target = fm.elliptical_kernel(), fm.conjugate_target(4)
+    with pytest.raises((ValueError, RuntimeError)):
+        fm.run_fsm_batched(bundle, target, fm.init_batch(bundle, target, 8, 0), 4, precision="fp32")

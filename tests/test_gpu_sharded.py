@@ -67,7 +67,7 @@ def worker(rank, world, port, name, q):
         m = _case(name, fm)[2]
         lo, hi = distributed.shard_range(m, rank, world)
         out = _run(fm, name, lo, hi, distributed.stop_sync())
-        if out[0] == "error":
+        if isinstance(out[0], str):        # ("error", chain, iteration, cause)
             q.put((rank, out))
         else:
             s, led = out
@@ -93,7 +93,7 @@ def _spawn(name, world=2):
         for _ in range(world):
             rank, out = q.get(timeout=240)
             res[rank] = out
-            if out[0] == "exception":     # the other rank may now wait in a collective
+            if isinstance(out[0], str) and out[0] == "exception":   # the other rank may wait in a collective
                 raise AssertionError(f"rank {rank} failed:\n{out[1]}")
     except queue.Empty:
         raise AssertionError(f"ranks {sorted(set(range(world)) - set(res))} sent nothing in 240 s")
@@ -125,9 +125,9 @@ def test_two_shards_reproduce_the_whole_batch(name):
 def test_first_failure_is_raised_on_every_rank():
     import paper_2503_17405_b200 as fm
     whole = _run(fm, "nan", 0, 40)
-    assert whole[0] == "error"
+    assert isinstance(whole[0], str) and whole[0] == "error"
     res = _spawn("nan")
     for rank, out in res.items():
-        assert out[0] == "error"
+        assert isinstance(out[0], str) and out[0] == "error"
         assert out[1:3] == whole[1:3], (rank, out, whole)
         assert out[3] == whole[3]
