@@ -127,9 +127,24 @@ __global__ void __launch_bounds__(256) drmh_draws_ilp_kernel(Params p) {
         }
       }
       __syncwarp();
-      for (int t = lane; t < nt; t += 32) {
-        const unsigned kk = qk[t];
-        out[kk & 0x7fffffffu] = ndtri_tail(qy[t], (kk >> 31) != 0);
+      // the queue two items per lane at a time (straight-line tail: the two
+      // dependency chains interleave); a chunk holds ~63 tails, so one pass
+#ifndef FSMC_TAIL_SL
+#define FSMC_TAIL_SL 1
+#endif
+      if (!FSMC_TAIL_SL) {
+        for (int t = lane; t < nt; t += 32) {
+          const unsigned kk = qk[t];
+          out[kk & 0x7fffffffu] = ndtri_tail(qy[t], (kk >> 31) != 0);
+        }
+      } else
+      for (int t = lane; t < nt; t += 64) {
+        const int t2 = t + 32 < nt ? t + 32 : t;
+        const unsigned k1 = qk[t], k2 = qk[t2];
+        const double v1 = ndtri_tail_sl(qy[t], (k1 >> 31) != 0);
+        const double v2 = ndtri_tail_sl(qy[t2], (k2 >> 31) != 0);
+        out[k1 & 0x7fffffffu] = v1;
+        out[k2 & 0x7fffffffu] = v2;
       }
       __syncwarp();
     }
