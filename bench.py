@@ -590,6 +590,34 @@ def lockstep_accounting(args, cfg, fm, bundle, target, m, n_lock, off, ledger, t
                                      "speedup": v_same / lock_value,
                                      "speedup_over_R": v_same / lock_value / r_of_m,
                                      "options": same}
+        if cfg["family"] == "drmh":
+            # R(m) = 1 exactly: max_tries = 1 makes every sample one proposal, so
+            # the lock-step / FSM ratio there is the synchronisation overhead alone
+            # (same generator, same chains); R(m) x this predicts the speed-up
+            b1 = fm.drmh_kernel(1, bundle.proposal_scale)
+            ts = {}
+            for kind in ("fsm", "lockstep"):
+                best = []
+                for s in range(2):
+                    barrier()
+                    bt = fm.init_batch(b1, target, m, 70 + s, chain_offset=off)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    if kind == "fsm":
+                        fm.run_fsm_batched(b1, target, bt, n_lock, step_variant=cfg["variant"],
+                                           output="torch", surplus=False, lanes=args.lanes)
+                    else:
+                        fm.run_standard_batched(b1, target, bt, n_lock, output="torch",
+                                                lanes=args.lanes)
+                    e1.record()
+                    barrier()
+                    best.append(e0.elapsed_time(e1))
+                ts[kind] = max_over_ranks(min(best) / 1e3)
+            ov = ts["lockstep"] / ts["fsm"]
+            out["sync_overhead_at_R1"] = {
+                "kernel": "drmh_kernel(max_tries=1): one proposal per sample, R(m) = 1",
+                "fsm_ms": 1e3 * ts["fsm"], "lockstep_ms": 1e3 * ts["lockstep"], "ratio": ov,
+                "predicted_speedup_same_generator": r_of_m * ov}
         batch = fm.init_batch(bundle, target, m, 60, chain_offset=off)
         bus = LS.lockstep_barrier_us(bundle, target, batch, lanes=args.lanes)
         out["barrier_us"] = bus

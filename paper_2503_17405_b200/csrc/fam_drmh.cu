@@ -73,8 +73,11 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
 #ifndef FSMC_GEN_U
 #define FSMC_GEN_U 4
 #endif
+#ifndef FSMC_GEN_MINB
+#define FSMC_GEN_MINB 1
+#endif
 template <int U>
-__global__ void __launch_bounds__(256) drmh_draws_ilp_kernel(Params p) {
+__global__ void __launch_bounds__(256, FSMC_GEN_MINB) drmh_draws_ilp_kernel(Params p) {
   __shared__ double qy_all[8][kDrawChunk];
   __shared__ unsigned qk_all[8][kDrawChunk];
   const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,10 +135,11 @@ __global__ void __launch_bounds__(256) drmh_draws_ilp_kernel(Params p) {
 #ifndef FSMC_TAIL_SL
 #define FSMC_TAIL_SL 1
 #endif
-      if (!FSMC_TAIL_SL) {
+      if (FSMC_TAIL_SL != 1) {
         for (int t = lane; t < nt; t += 32) {
           const unsigned kk = qk[t];
-          out[kk & 0x7fffffffu] = ndtri_tail(qy[t], (kk >> 31) != 0);
+          out[kk & 0x7fffffffu] = FSMC_TAIL_SL == 2 ? ndtri_tail_sl(qy[t], (kk >> 31) != 0)
+                                                    : ndtri_tail(qy[t], (kk >> 31) != 0);
         }
       } else
       for (int t = lane; t < nt; t += 64) {
