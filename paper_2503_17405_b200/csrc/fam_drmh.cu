@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256, FSMC_GEN_MINB) drmh_draws_ilp_kernel(Para
       // the queue two items per lane at a time (straight-line tail: the two
       // dependency chains interleave); a chunk holds ~63 tails, so one pass
 #ifndef FSMC_TAIL_SL
-#define FSMC_TAIL_SL 1
+#define FSMC_TAIL_SL 2
 #endif
       if (FSMC_TAIL_SL != 1) {
         for (int t = lane; t < nt; t += 32) {
