@@ -376,6 +376,14 @@ int64_t fsmc_gp_lml_max_rows(void);   /* n limit of fsmc_gp_lml (shared memory) 
 fsmc_status fsmc_gp_lml(const double* theta, int64_t k, const double* d2, const double* y, int64_t n,
                         double jitter, int32_t residual, double* work, int64_t work_slots, double* lp,
                         void* stream_);
+/* The same with the gradient: grad [k][3] (or NULL for values only) gets the
+ * reference's trace form (targets.py:238-254) from the factor the value pass
+ * left in the workspace slot -- alpha = K^-1 y, W = L^-1 in the slot's upper
+ * half, tr(K^-1), tr(K^-1 E) and tr(K^-1 (E o D2)) as sums of quadratic forms
+ * in the rows of W -- minus theta unless `residual`.  No library call. */
+fsmc_status fsmc_gp_lml_grad(const double* theta, int64_t k, const double* d2, const double* y, int64_t n,
+                             double jitter, int32_t residual, double* work, int64_t work_slots, double* lp,
+                             double* grad, void* stream_);
 const char* fsmc_gp_last_error(void);
 
 /* Cross-chain diagnostic partials for effective_sample_size / R-hat

@@ -117,6 +117,9 @@ def lib():
     L.fsmc_gp_lml.restype = S
     L.fsmc_gp_lml.argtypes = [_P, ctypes.c_int64, _P, _P, ctypes.c_int64, _D, ctypes.c_int32, _P,
                               ctypes.c_int64, _P, _P]
+    L.fsmc_gp_lml_grad.restype = S
+    L.fsmc_gp_lml_grad.argtypes = [_P, ctypes.c_int64, _P, _P, ctypes.c_int64, _D, ctypes.c_int32, _P,
+                                   ctypes.c_int64, _P, _P, _P]
     L.fsmc_gp_last_error.restype = ctypes.c_char_p
     L.fsmc_gp_lml_max_rows.restype = ctypes.c_int64
     L.fsmc_advance_lockstep.restype = S

@@ -73,11 +73,18 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
 #ifndef FSMC_GEN_U
 #define FSMC_GEN_U 4
 #endif
+// register budget: ptxas's default for (256) threads (64 registers) measured
+// fastest; FSMC_GEN_MINB > 0 forces a minimum number of resident blocks
 #ifndef FSMC_GEN_MINB
-#define FSMC_GEN_MINB 1
+#define FSMC_GEN_MINB 0
+#endif
+#if FSMC_GEN_MINB > 0
+#define FSMC_GEN_BOUNDS __launch_bounds__(256, FSMC_GEN_MINB)
+#else
+#define FSMC_GEN_BOUNDS __launch_bounds__(256)
 #endif
 template <int U>
-__global__ void __launch_bounds__(256, FSMC_GEN_MINB) drmh_draws_ilp_kernel(Params p) {
+__global__ void FSMC_GEN_BOUNDS drmh_draws_ilp_kernel(Params p) {
   __shared__ double qy_all[8][kDrawChunk];
   __shared__ unsigned qk_all[8][kDrawChunk];
   const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -195,9 +195,12 @@ class GPHyperEvaluator:
         K_j = tau_j^2 exp(-lam_j^2 D2) + (sigma_j^2 + jitter) I     [k, n, n]
         L_j = chol(K_j),  alpha_j = K_j^-1 y,  lml_j = -y.alpha_j/2 - sum log diag L_j - n log(2 pi)/2
 
-    by ``fsmc_gp_lml`` (csrc/gp_chol.cu: one CTA per chain, a left-looking
-    blocked Cholesky with K formed on the fly) for values, and by batched
-    fp64 factorizations (torch.linalg) where the gradient is needed.  ``residual=True`` returns the marginal likelihood (the
+    by ``fsmc_gp_lml_grad`` (csrc/gp_chol.cu: one CTA per chain, a
+    left-looking blocked Cholesky with K formed on the fly; with the
+    gradient, alpha = K^-1 y, W = L^-1 and the trace terms from the same
+    factor).  ``torch_eval`` (batched torch.linalg factorizations) is kept as
+    a cross-check and for single-request value rounds, which one matrix
+    spread over the whole GPU serves faster.  ``residual=True`` returns the marginal likelihood (the
     elliptical kernel's residual log density); otherwise the N(0, I) prior
     terms are added.  The gradient is the reference's trace form with
     A = alpha alpha^T - K^-1.  A kernel matrix that is not positive definite
@@ -213,24 +216,24 @@ class GPHyperEvaluator:
         self.min_kernel_rows = 16
 
     def __call__(self, theta, lp, g=None):
-        # value only, enough requests to fill the SMs: the hand-written kernel
-        # (csrc/gp_chol.cu, one CTA per chain); a handful of requests runs
-        # faster through the library factorization, which spreads one matrix
-        # over the whole GPU
-        if g is None and theta.shape[0] >= self.min_kernel_rows and \
-                self.n <= _lib.lib().fsmc_gp_lml_max_rows():
-            if self.work is None:
-                self.work = torch.empty((self.slots, self.n, self.n), dtype=torch.float64,
-                                        device=self.d2.device)
-            theta = theta.contiguous()
-            st = _lib.lib().fsmc_gp_lml(theta.data_ptr(), theta.shape[0], self.d2.data_ptr(),
-                                        self.y.data_ptr(), self.n, self.jitter, int(self.residual),
-                                        self.work.data_ptr(), self.slots, lp.data_ptr(),
-                                        _lib.stream_ptr())
-            if st != 0:
-                raise _lib.EngineError(_lib.lib().fsmc_gp_last_error().decode())
-            return
-        self.torch_eval(theta, lp, g)
+        # the hand-written kernel (csrc/gp_chol.cu, one CTA per chain) for every
+        # gradient round and for value rounds with enough requests to fill the
+        # SMs; a handful of value requests runs faster through the library
+        # factorization, which spreads one matrix over the whole GPU
+        if self.n > _lib.lib().fsmc_gp_lml_max_rows():
+            return self.torch_eval(theta, lp, g)
+        if g is None and theta.shape[0] < self.min_kernel_rows:
+            return self.torch_eval(theta, lp, g)
+        if self.work is None:
+            self.work = torch.empty((self.slots, self.n, self.n), dtype=torch.float64,
+                                    device=self.d2.device)
+        theta = theta.contiguous()
+        st = _lib.lib().fsmc_gp_lml_grad(theta.data_ptr(), theta.shape[0], self.d2.data_ptr(),
+                                         self.y.data_ptr(), self.n, self.jitter, int(self.residual),
+                                         self.work.data_ptr(), self.slots, lp.data_ptr(),
+                                         _lib.ptr(g), _lib.stream_ptr())
+        if st != 0:
+            raise _lib.EngineError(_lib.lib().fsmc_gp_last_error().decode())
 
     def torch_eval(self, theta, lp, g=None):
         """Value (and gradient) through torch.linalg's batched factorizations
