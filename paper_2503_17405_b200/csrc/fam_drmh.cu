@@ -195,8 +195,12 @@ cudaError_t dispatch_drmh(int op, int g, int e, Params& p, const LaunchCtx& lc, 
 #undef X
       return cudaErrorInvalidConfiguration;
     }
-#define S(GG, EE, TK) \
-  if (g == GG && e == EE && kind == TK) return Launch<DrmhW, GG, EE, TK>::window(p, lc, s);
+    // the benchmark plugins at their exact dimension (G * E): guard-free kernels
+#define S(GG, EE, TK)                                                                 \
+  if (g == GG && e == EE && kind == TK) {                                             \
+    if (p.t.dim == GG * EE) return Launch<DrmhWX, GG, EE, TK>::window(p, lc, s);      \
+    return Launch<DrmhW, GG, EE, TK>::window(p, lc, s);                               \
+  }
     FSMC_DRMH_SPECIAL(S)
 #undef S
 #define X(GG, EE) \
@@ -212,8 +216,11 @@ cudaError_t dispatch_drmh(int op, int g, int e, Params& p, const LaunchCtx& lc, 
 #undef X
     return cudaErrorInvalidConfiguration;
   }
-#define S(GG, EE, TK) \
-  if (g == GG && e == EE && kind == TK) return launch_op<Drmh, GG, EE, TK>(op, p, lc, s, ps, off, x0, jit);
+#define S(GG, EE, TK)                                                                            \
+  if (g == GG && e == EE && kind == TK) {                                                        \
+    if (op == 1 && p.t.dim == GG * EE) return Launch<DrmhX, GG, EE, TK>::run(p, lc, s);          \
+    return launch_op<Drmh, GG, EE, TK>(op, p, lc, s, ps, off, x0, jit);                          \
+  }
   if (op != 0) {
     FSMC_DRMH_SPECIAL(S)
   }
