@@ -175,6 +175,19 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                      int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
                      const fsmc_outputs* out, int32_t lanes, void* stream_);
 
+/* fsmc_run with sample egress: `host_samples` (pinned host memory,
+ * [n][m][dim], or NULL) receives out->samples.  With parts > 1 the chains run
+ * in `parts` contiguous parts launched back to back on two streams (each
+ * part's blocks backfill the SMs the previous part's tail frees) and every
+ * finished part's sample columns are copied to the host (one pitched copy)
+ * on a device-owned egress stream while later parts still run; parts <= 1
+ * copies after the run.  Results are identical to fsmc_run (chains are
+ * independent).  The copies are ordered before later work on `stream`. */
+fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                            int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                            const fsmc_outputs* out, int32_t lanes, int32_t parts, double* host_samples,
+                            void* stream);
+
 /* Replaces run_standard_batched (lockstep.py:238-305): the lock-step
  * (vmap-style) baseline built from the same device blocks.  Every inner-loop
  * iteration ends at a grid-wide barrier, so a sample costs max over chains of

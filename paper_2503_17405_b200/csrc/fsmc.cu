@@ -448,6 +448,13 @@ fsmc_status fsmc_init_finish(const fsmc_kernel* k, const fsmc_target* t, fsmc_st
 fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n, int32_t variant,
                      const int32_t* order, int64_t tick_limit, int32_t mode, const fsmc_outputs* out,
                      int32_t lanes, void* stream_) {
+  return fsmc_run_egress(k, t, st, n, variant, order, tick_limit, mode, out, lanes, 1, nullptr, stream_);
+}
+
+fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
+                            int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
+                            const fsmc_outputs* out, int32_t lanes, int32_t parts, double* host_samples,
+                            void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (n < 0) return fail(FSMC_ERR_ARG, "n must be >= 0");
@@ -472,9 +479,53 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
     if (p.order[i] != (i == 0 ? K : i)) p.default_order = 0;
   }
   cudaStream_t cs = (cudaStream_t)stream_;
-  p.next_chain = st->work;
-  CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
-  CUDA_TRY(dispatch_family(1, ge, p, cs));
+  p.j_lo = 0;
+  p.j_hi = st->m;
+  if (!host_samples || !out || !out->samples || n <= 0 || parts <= 1 || st->m < 2 * parts) {
+    p.next_chain = st->work;
+    CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
+    CUDA_TRY(dispatch_family(1, ge, p, cs));
+    if (host_samples && out && out->samples && n > 0)
+      CUDA_TRY(cudaMemcpyAsync(host_samples, out->samples, (size_t)n * st->m * t->dim * sizeof(double),
+                               cudaMemcpyDeviceToHost, cs));
+    return FSMC_OK;
+  }
+  // chains in `parts` contiguous parts launched back to back on two alternating
+  // streams (a part's blocks backfill the SMs the previous part's tail frees);
+  // each finished part's sample columns go to the host on the egress stream
+  // (one pitched copy: n rows of its chains) while later parts still run
+  if (parts > kMaxParts) parts = kMaxParts;
+  cudaStream_t side[kMaxParts] = {};
+  CUDA_TRY(side_streams(side));
+  cudaStream_t comp[2] = {cs, side[1]};
+  cudaEvent_t ev_fork, ev_part[kMaxParts], ev_done;
+  CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+  for (int h = 0; h < parts; h++) CUDA_TRY(cudaEventCreateWithFlags(&ev_part[h], cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(ev_fork, cs));
+  CUDA_TRY(cudaStreamWaitEvent(side[1], ev_fork, 0));
+  CUDA_TRY(cudaStreamWaitEvent(side[0], ev_fork, 0));
+  const size_t row = (size_t)st->m * t->dim * sizeof(double);
+  for (int h = 0; h < parts; h++) {
+    Params ph = p;
+    ph.j_lo = st->m * h / parts;
+    ph.j_hi = st->m * (h + 1) / parts;
+    ph.next_chain = st->work + 16 * h;
+    cudaStream_t sh = comp[h & 1];
+    CUDA_TRY(cudaMemsetAsync(ph.next_chain, 0, sizeof(unsigned), sh));
+    CUDA_TRY(dispatch_family(1, ge, ph, sh));
+    CUDA_TRY(cudaEventRecord(ev_part[h], sh));
+    CUDA_TRY(cudaStreamWaitEvent(side[0], ev_part[h], 0));
+    const size_t off = (size_t)ph.j_lo * t->dim * sizeof(double);
+    CUDA_TRY(cudaMemcpy2DAsync((char*)host_samples + off, row, (const char*)out->samples + off, row,
+                               (size_t)(ph.j_hi - ph.j_lo) * t->dim * sizeof(double), (size_t)n,
+                               cudaMemcpyDeviceToHost, side[0]));
+  }
+  CUDA_TRY(cudaEventRecord(ev_done, side[0]));
+  CUDA_TRY(cudaStreamWaitEvent(cs, ev_done, 0));   // the egress waited on every part
+  CUDA_TRY(cudaEventDestroy(ev_fork));
+  CUDA_TRY(cudaEventDestroy(ev_done));
+  for (int h = 0; h < parts; h++) CUDA_TRY(cudaEventDestroy(ev_part[h]));
   return FSMC_OK;
 }
 

@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run
   Grp<G> grp;
   double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
   double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
-  while (true) {
+  while (true) {   // chains [j_lo, j_hi) of the state block (fsmc_run_egress runs it in parts)
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
-    j = grp.bcast_ll(j, 0);
-    if (j >= p.st.m) break;
+    j = p.j_lo + grp.bcast_ll(j, 0);
+    if (j >= p.j_hi) break;
     Core c;
     core_load(c, p, j);
     c.ws = ws;
@@ -473,8 +473,8 @@ struct Launch {
   }
   static cudaError_t run(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     if constexpr (TK != 0)
-      if (unrolled(p)) return persistent(fsm_run_kernel<F, G, E, TK, 1>, p, lc, s);
-    return persistent(fsm_run_kernel<F, G, E, TK, 0>, p, lc, s);
+      if (unrolled(p)) return persistent(fsm_run_kernel<F, G, E, TK, 1>, p, lc, s, 0, p.j_hi - p.j_lo);
+    return persistent(fsm_run_kernel<F, G, E, TK, 0>, p, lc, s, 0, p.j_hi - p.j_lo);
   }
   static cudaError_t profile(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     return persistent(fsm_profile_kernel<F, G, E>, p, lc, s);

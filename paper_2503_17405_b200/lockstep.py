@@ -492,9 +492,16 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
             egressed = egressed or dst is not None
     elif evaluator is None:
         def launch(mode, tick_limit):
-            _lib.check(lib.fsmc_run(ctypes.byref(kern), ctypes.byref(tgt),
-                                    ctypes.byref(batch.struct()), n, variant, ordv, tick_limit, mode,
-                                    ctypes.byref(out), lanes, _lib.stream_ptr()), "fsmc_run")
+            nonlocal egressed
+            dst = host.data_ptr() if host is not None and mode == 0 else None
+            # chains in parts of >= 2048 (about a resident wave): each finished
+            # part's samples stream to the host while the next parts run
+            parts = max(1, min(8, m // 2048)) if dst else 1
+            _lib.check(lib.fsmc_run_egress(ctypes.byref(kern), ctypes.byref(tgt),
+                                           ctypes.byref(batch.struct()), n, variant, ordv, tick_limit,
+                                           mode, ctypes.byref(out), lanes, parts, dst,
+                                           _lib.stream_ptr()), "fsmc_run_egress")
+            egressed = egressed or dst is not None
     else:
         launch = _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evaluator)
 

@@ -64,3 +64,18 @@ def test_two_batches_on_two_streams_equal_serial_runs(fm):
         assert (res[mode][1] > 0).all() and (res[mode][3] > 0).all()
     for x, y in zip(res["serial"], res["concurrent"]):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("m", [4096, 16384])
+def test_streamed_host_output_equals_device_output(fm, m):
+    """output="numpy" streams finished chain parts to pinned host memory
+    during the run (fsmc_run_egress); the samples and ledger equal the
+    device-resident run's."""
+    bundle, target = fm.nuts_kernel(0.05, 10), fm.equicorrelated_gaussian_target(100, 0.99)
+    n = 12
+    a, la = fm.run_fsm_batched(bundle, target, fm.init_batch(bundle, target, m, 4), n,
+                               step_variant="bundled", output="numpy", surplus=False)
+    b, lb = fm.run_fsm_batched(bundle, target, fm.init_batch(bundle, target, m, 4), n,
+                               step_variant="bundled", output="torch", surplus=False)
+    assert np.array_equal(a, b.cpu().numpy())
+    assert np.array_equal(la.iter_counts, lb.iter_counts.cpu().numpy())
