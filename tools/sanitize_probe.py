@@ -20,13 +20,13 @@ def main():
 
     mog = fm.correlated_mog_target(10, 0.9, [-3.0, 0.0, 3.0])
     dr = fm.drmh_kernel(20, 0.3)
-    a, la = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 6, step_variant="bundled")
-    b, lb = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 6, step_variant="bundled",
+    a, la = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 12, step_variant="bundled")
+    b, lb = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 12, step_variant="bundled",
                                draw_window=220, draw_parts=2)
     assert np.array_equal(a, b), "windowed run differs"
     c, lc = fm.run_standard_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 6)
     assert np.array_equal(a, c), "lock-step differs"
-    f32, _ = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 6, step_variant="bundled",
+    f32, _ = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 12, step_variant="bundled",
                                 precision="fp32")
     assert np.isfinite(f32).all()
     print("drmh ok")
@@ -56,7 +56,7 @@ def main():
     assert bool(torch.isfinite(lp).all()) and bool(torch.isfinite(g).all())
     print("logreg_tc ok")
 
-    ess = fm.effective_sample_size(a[2:], burn=0)
+    ess = fm.effective_sample_size(a, burn=0)
     assert np.isfinite(ess.pooled)
     print("diagnostics ok")
 
