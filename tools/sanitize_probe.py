@@ -24,7 +24,7 @@ def main():
     b, lb = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 12, step_variant="bundled",
                                draw_window=220, draw_parts=2)
     assert np.array_equal(a, b), "windowed run differs"
-    c, lc = fm.run_standard_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 6)
+    c, lc = fm.run_standard_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 12)
     assert np.array_equal(a, c), "lock-step differs"
     f32, _ = fm.run_fsm_batched(dr, mog, fm.init_batch(dr, mog, 96, 1), 12, step_variant="bundled",
                                 precision="fp32")
