@@ -126,6 +126,7 @@ __global__ void FSMC_GEN_BOUNDS drmh_draws_ilp_kernel(Params p) {
           const bool live = k < c1;
           const double v = uni[u] ? bd[u] * INV_2_53 : vc[u];     // prng.py:97-100
           const bool tail = live && !uni[u] && !cen[u];
+          FSMC_CHECK(!live || k < W);
           if (live && !tail) out[k] = v;
           const unsigned bt = __ballot_sync(0xffffffffu, tail);
           if (tail) {
@@ -145,6 +146,7 @@ __global__ void FSMC_GEN_BOUNDS drmh_draws_ilp_kernel(Params p) {
       if (FSMC_TAIL_SL != 1) {
         for (int t = lane; t < nt; t += 32) {
           const unsigned kk = qk[t];
+          FSMC_CHECK((int)(kk & 0x7fffffffu) < W && nt <= kDrawChunk);
           out[kk & 0x7fffffffu] = FSMC_TAIL_SL == 2 ? ndtri_tail_sl(qy[t], (kk >> 31) != 0)
                                                     : ndtri_tail(qy[t], (kk >> 31) != 0);
         }

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_win
     if (c.count >= n_stop || c.tick >= p.tick_limit) continue;
     c.dw = p.draws + (size_t)j * p.window;
     c.dbase = c.ctr;
+    c.dlim = p.window;
     F<G, E> f;
     f.load(p, j, grp);
     bool ok = true;
