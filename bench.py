@@ -444,18 +444,19 @@ def main():
     # This engine keeps that state on chip, so it is the bandwidth-equivalent
     # rate of the state-model, not DRAM traffic (that is `traffic`).
     n_inner = int(ledger.iter_counts.sum().item()) if hasattr(ledger.iter_counts, "sum") else 0
+    fp = 4 if cfg.get("precision") == "fp32" else 8     # 8(d): bytes per float, parity / throughput
     if cfg["family"] == "ess":
-        units, per_unit, uname = n_inner + 2 * n * m, 2 * d * 8 + 96 + 3 * d * 8 * n * m / \
+        units, per_unit, uname = n_inner + 2 * n * m, 2 * d * fp + 96 + 3 * d * fp * n * m / \
             max(1, n_inner + 2 * n * m), "chain-tick (INIT, SHRINK, DONE)"
     elif cfg["family"] == "nuts":
-        units, per_unit, uname = n_inner, 9.3 * d * 8 + 100, "INTEGRATE chain-tick (leapfrog)"
+        units, per_unit, uname = n_inner, 9.3 * d * fp + 100, "INTEGRATE chain-tick (leapfrog)"
     else:
-        units, per_unit, uname = n_inner, 2 * d * 8 + 96 + 2 * d * 8 * n * m / max(1, n_inner), \
+        units, per_unit, uname = n_inner, 2 * d * fp + 96 + 2 * d * fp * n * m / max(1, n_inner), \
             "PROPOSE chain-tick"
     sm_ach = units * per_unit / (kms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": sm_ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": sm_ach / peaks["hbm_gbs"], "traffic": None,
-            "kernel": ("drmh_draws_kernel + fsm_window_kernel<DrmhW,1,10,MOG>" if win else
+            "kernel": ("drmh_draws_ilp_kernel<4> + fsm_window_kernel<DrmhWX,1,10,MOG,1>" if win else
                        "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel"),
             "kernel_ms": kms, "unit_of_work": uname, "units": units, "bytes_per_unit": per_unit,
             "algorithmic_bytes": units * per_unit,
@@ -481,15 +482,21 @@ def main():
             % t["measured_bytes_per_chain_sample"]
     if cfg["family"] == "drmh" and proposals:
         # executed fp64 flops per DRMH proposal (DFMA = 2), from ncu SASS counts of
-        # this pair of kernels (profiles/r01b_c2_ncu.md); peak = measured DFMA rate
-        fl = FP64_FLOPS_PER_PROPOSAL * proposals
+        # this pair of kernels (profiles/r04_c2_issue.json when present); peak =
+        # measured DFMA rate
+        ip = os.path.join(ROOT, "profiles", ISSUE_PROFILE)
+        fpp, fsrc = FP64_FLOPS_PER_PROPOSAL, "profiles/r01b_c2_ncu.md"
+        if win and cfg.get("precision") != "fp32" and os.path.exists(ip):
+            t = json.load(open(ip))
+            if t.get("fp64_flops_per_proposal"):
+                fpp, fsrc = t["fp64_flops_per_proposal"], "profiles/" + ISSUE_PROFILE
+        fl = fpp * proposals
         ach_tf = fl / (kms / 1e3) / 1e12
         roof["compute"] = {"pipe": "fp64", "achieved": ach_tf, "peak": pipe["fp64_fma_tflops"],
                            "unit": "TFLOP/s", "frac": ach_tf / pipe["fp64_fma_tflops"],
-                           "flops_per_proposal": FP64_FLOPS_PER_PROPOSAL, "proposals": proposals,
+                           "flops_per_proposal": fpp, "flops_source": fsrc, "proposals": proposals,
                            "peak_source": "profiles/r01_pipe_peaks.json (tools/peak_probe.cu)"}
-        ip = os.path.join(ROOT, "profiles", ISSUE_PROFILE)
-        if win and os.path.exists(ip):
+        if win and cfg.get("precision") != "fp32" and os.path.exists(ip):
             # warp instructions per proposal of the two kernels (ncu sm__inst_executed
             # over a profiled run / that run's proposals) against the issue ceiling:
             # 148 SMs x 4 schedulers x one warp instruction per cycle at this run's clock

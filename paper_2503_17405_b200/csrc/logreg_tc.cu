@@ -286,6 +286,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
       const long long r0 = (long long)i * BN + half * COLS;
       const int valid = r0 + COLS <= N ? COLS : (int)(N > r0 ? N - r0 : 0);
+#ifndef FSMC_SP_POLY
+#define FSMC_SP_POLY 1
+#endif
+#if FSMC_SP_POLY
+      // two MUFU operations per element (ex2, rcp) instead of three: with
+      // e = 2^(-|z| log2 e) in (0, 1], softplus(z) = max(z, 0) + log1p(e) with
+      // log1p on the FMA pipe (degree-8 minimax-like fit of log1p(e)/e on [0, 1],
+      // |error| < 2e-7, mean bias 1e-8), sigmoid(z) = r or 1 - r, r = 1/(1 + e).
+      // The epilogue was MUFU-bound (3 ops x 8192 elements per tile against
+      // the tile's ~1100 tensor cycles); now MUFU and tensor balance.
+      auto element = [&](float zz, float& sig) -> float {
+        float en, r;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(en) : "f"(-1.4426950408889634f * fabsf(zz)));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + en));
+        sig = zz >= 0.0f ? r : 1.0f - r;
+        float q = 5.186003710e-03f;
+        q = fmaf(q, en, -2.921026794e-02f);
+        q = fmaf(q, en, 7.754038125e-02f);
+        q = fmaf(q, en, -1.358394190e-01f);
+        q = fmaf(q, en, 1.905595565e-01f);
+        q = fmaf(q, en, -2.482564859e-01f);
+        q = fmaf(q, en, 3.331601067e-01f);
+        q = fmaf(q, en, -4.999925590e-01f);
+        q = fmaf(q, en, 9.999999209e-01f);
+        return fmaf(q, en, fmaxf(zz, 0.0f));
+      };
+#else
       auto element = [&](float zz, float& sig) -> float {
         const float zc = fmaxf(zz, -87.0f);
         float en, l2;
@@ -295,6 +322,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(ope));
         return fmaf(0.6931471805599453f, l2, zc);
       };
+#endif
       if (valid == COLS) {
 #pragma unroll
         for (int c = 0; c < COLS; c += 2) {

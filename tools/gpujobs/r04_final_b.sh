@@ -1,8 +1,13 @@
 # round 2 final (b): ncu launch lists and full captures of the headline kernels (C2), the
 # C2 instruction counts, C4/C5 launch lists
 mkdir -p gpurun_out/r04f_b
+# C5 epilogue: log1p on the FMA pipe (two MUFU ops per element) vs the three-MUFU form
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "fused" > gpurun_out/r04f_b/fused_tests.log 2>&1; tail -1 gpurun_out/r04f_b/fused_tests.log
+for L in paper_2503_17405_b200/libfsmc.so variants/sp0/libfsmc.so paper_2503_17405_b200/libfsmc.so; do
+  echo $L; FSMC_LIB=$(realpath $L) timeout 300 python tools/tc_probe.py 131072 fp16-tc 3; FSMC_LIB=$(realpath $L) timeout 300 python tools/tc_probe.py 18944 fp16-tc 5
+done > gpurun_out/r04f_b/c5_epilogue_ab.txt 2>&1; cat gpurun_out/r04f_b/c5_epilogue_ab.txt
 timeout 600 python tools/issue_probe.py 200 > gpurun_out/r04f_b/plain_probe.json 2>&1 && \
-timeout 600 ncu --metrics sm__inst_executed.sum,gpu__time_duration.sum,smsp__cycles_active.avg --clock-control none \
+timeout 600 ncu --metrics sm__inst_executed.sum,gpu__time_duration.sum,smsp__cycles_active.avg,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dfma_pred_on.sum --clock-control none \
   -k regex:"drmh_draws|fsm_window" --csv --log-file gpurun_out/r04f_b/c2_issue.csv python tools/issue_probe.py 200 > gpurun_out/r04f_b/c2_issue_probe.json 2> gpurun_out/r04f_b/c2_issue.err
 python tools/issue_probe.py --summarise gpurun_out/r04f_b/c2_issue.csv gpurun_out/r04f_b/c2_issue_probe.json > gpurun_out/r04f_b/r04_c2_issue.json 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r04f_b/c2_launches.csv \

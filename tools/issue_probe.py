@@ -2,7 +2,9 @@
 that prints its proposal count; under `ncu --metrics sm__inst_executed.sum,...`
 it yields the warp instructions per DRMH proposal of the two hot kernels.
 
-  ncu --metrics sm__inst_executed.sum,gpu__time_duration.sum,smsp__cycles_active.avg \
+  ncu --metrics sm__inst_executed.sum,gpu__time_duration.sum,smsp__cycles_active.avg,\
+      sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,\
+      sm__sass_thread_inst_executed_op_dfma_pred_on.sum \
       -k regex:"drmh_draws|fsm_window" --csv --log-file X.csv python tools/issue_probe.py 200 > P.json
   python tools/issue_probe.py --summarise X.csv P.json > profiles/r04_c2_issue.json
 """
@@ -43,12 +45,20 @@ def summarise(csv_path, probe_path):
         if r["Metric Name"] == "sm__inst_executed.sum":
             launches[k] += 1
     per = {k: agg[k]["sm__inst_executed.sum"] / probe["proposals"] for k in agg}
+    dp = {}
+    for k in agg:   # executed fp64 flops (DFMA counted twice) per proposal
+        a = agg[k]
+        dp[k] = (a.get("sm__sass_thread_inst_executed_op_dadd_pred_on.sum", 0.0) +
+                 a.get("sm__sass_thread_inst_executed_op_dmul_pred_on.sum", 0.0) +
+                 2 * a.get("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", 0.0)) / probe["proposals"]
     out = {"what": "warp instructions executed per DRMH proposal (C2: MoG d=10, m=65536, "
                    "windowed draws in 4 parts), ncu sm__inst_executed.sum over every launch of "
                    "the profiled run / its proposals",
            "probe": probe, "launches": dict(launches),
            "warp_inst_per_proposal_by_kernel": per,
            "warp_inst_per_proposal": sum(per.values()),
+           "fp64_flops_per_proposal_by_kernel": dp,
+           "fp64_flops_per_proposal": sum(dp.values()),
            "totals": {k: dict(v) for k, v in agg.items()},
            "command": "tools/issue_probe.py (see its docstring)"}
     print(json.dumps(out, indent=1))
