@@ -188,6 +188,12 @@ fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_sta
                             const fsmc_outputs* out, int32_t lanes, int32_t parts, double* host_samples,
                             void* stream);
 
+/* Device -> host copy of `rows` rows of `width` bytes, both sides with row
+ * pitch `pitch` (a chain range's columns of samples [n][m][dim]), ordered on
+ * `stream`: the sample egress of the batched prior-transform rounds. */
+fsmc_status fsmc_copy_to_host_2d(void* dst, const void* src, int64_t pitch, int64_t width, int64_t rows,
+                                 void* stream);
+
 /* Replaces run_standard_batched (lockstep.py:238-305): the lock-step
  * (vmap-style) baseline built from the same device blocks.  Every inner-loop
  * iteration ends at a grid-wide barrier, so a sample costs max over chains of

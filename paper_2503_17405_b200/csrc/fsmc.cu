@@ -889,6 +889,15 @@ fsmc_status fsmc_lockstep_barrier_probe(const fsmc_kernel* k, const fsmc_target*
   return FSMC_OK;
 }
 
+fsmc_status fsmc_copy_to_host_2d(void* dst, const void* src, int64_t pitch, int64_t width, int64_t rows,
+                                 void* stream_) {
+  if (!dst || !src || pitch < width || width < 0 || rows < 0) return fail(FSMC_ERR_ARG, "bad 2-D copy");
+  if (!rows || !width) return FSMC_OK;
+  CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)pitch, src, (size_t)pitch, (size_t)width, (size_t)rows,
+                             cudaMemcpyDeviceToHost, (cudaStream_t)stream_));
+  return FSMC_OK;
+}
+
 fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, double* lp, double* grad,
                              int32_t family, int32_t lanes, void* stream_) {
   if (!t || !X || !lp || m < 0) return fail(FSMC_ERR_ARG, "bad target_eval args");

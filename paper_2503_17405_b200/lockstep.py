@@ -474,7 +474,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
             prior_transform = None      # identity prior: nu = eps, nothing to batch
     if prior_transform is not None:
         launch = _prior_launcher(target, batch, n, variant, ordv, out, lanes, prior_transform,
-                                 prior_parts)
+                                 prior_parts, samples, host)
+        egressed = host is not None
     elif draw_window:
         # [m][window] plus a line of slack: the step kernel prefetches the
         # next proposal's draws, which for the last chain may lie past its window
@@ -633,13 +634,21 @@ def _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evalu
 
 
 _SIDE_STREAMS: dict = {}      # per device, reused across runs (prior_parts)
+_EGRESS_STREAMS: dict = {}    # per device: device -> host sample copies
 
 
-def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, parts=1):
+def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, parts=1,
+                    samples=None, host=None):
     """Rounds of fsmc_advance_prior + one batched nu = L eps over every
     chain parked at INIT.  parts > 1: the chains in contiguous parts, each
     with its own rounds on its own stream (fsmc_advance_prior_part), so one
-    part's transform overlaps another part's advance kernel."""
+    part's transform overlaps another part's advance kernel.
+
+    ``host`` (pinned, output="numpy"): a round completes one sample of every
+    chain of its part (each chain runs from one INIT park to the next), so
+    after a part's t-th advance its sample rows [0, t) are final and go to
+    the host (one pitched copy per round) on an egress stream while the
+    rounds continue."""
     m, d = batch.m, target.dim
     parts = max(1, min(int(parts), 8, m))
     bounds = [(m * h // parts, m * (h + 1) // parts) for h in range(parts)]
@@ -677,9 +686,28 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
             req_count[h:].data_ptr(), lanes, lo, hi, h, _lib.stream_ptr()),
             "fsmc_advance_prior_part")
 
+    egress = _EGRESS_STREAMS.setdefault(main.device, torch.cuda.Stream(device=main.device)) \
+        if host is not None else None
+    pitch = m * d * 8
+
+    def send(h, upto, sent):
+        """rows [sent[h], upto) of part h's chain columns to the host"""
+        if egress is None or upto <= sent[h]:
+            return
+        lo, hi = bounds[h]
+        off = sent[h] * pitch + lo * d * 8
+        _lib.check(lib.fsmc_copy_to_host_2d(host.data_ptr() + off, samples.data_ptr() + off, pitch,
+                                            (hi - lo) * d * 8, upto - sent[h], egress.cuda_stream),
+                   "fsmc_copy_to_host_2d")
+        sent[h] = upto
+
     def launch(mode, tick_limit):
         for s in streams[1:]:
             s.wait_stream(main)
+        if egress is not None:
+            egress.wait_stream(main)
+        sent = [0] * parts
+        done = [0] * parts           # advance calls completed per part
         active = list(range(parts))
         for h in active:
             with torch.cuda.stream(streams[h]):
@@ -688,8 +716,13 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
             still = []
             for h in active:
                 with torch.cuda.stream(streams[h]):
-                    k = int(req_count[h].item())
+                    k = int(req_count[h].item())     # this part's advance has finished
+                    if mode == 0:
+                        send(h, min(done[h], n), sent)
+                    done[h] += 1
                     if k == 0:
+                        if mode == 0:
+                            send(h, n, sent)
                         continue
                     stats["rounds"] += 1
                     stats["prior_transforms"] += k
@@ -700,6 +733,8 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
             active = still
         for s in streams[1:]:
             main.wait_stream(s)
+        if egress is not None:
+            main.wait_stream(egress)
 
     launch.stats = stats
     return launch

@@ -79,3 +79,20 @@ def test_streamed_host_output_equals_device_output(fm, m):
                                step_variant="bundled", output="torch", surplus=False)
     assert np.array_equal(a, b.cpu().numpy())
     assert np.array_equal(la.iter_counts, lb.iter_counts.cpu().numpy())
+
+
+def test_streamed_host_output_of_the_prior_transform_rounds(fm):
+    """The batched prior-transform rounds (C4's path) send each round's
+    finished sample rows of every chain part to pinned host memory while the
+    rounds continue; the result equals the device-resident run's."""
+    bundle, target = fm.elliptical_kernel(), fm.gp_classification_target(256)
+    m, n = 600, 15
+    runs = []
+    for output in ("numpy", "torch"):
+        s, led = fm.run_fsm_batched(bundle, target, fm.init_batch(bundle, target, m, 8), n,
+                                    step_variant="amortized", output=output, surplus=False,
+                                    prior_transform="dmma", prior_parts=3)
+        runs.append((np.asarray(s) if output == "numpy" else s.cpu().numpy(),
+                     np.asarray(led.iter_counts) if output == "numpy" else led.iter_counts.cpu().numpy()))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])

@@ -1,5 +1,5 @@
-"""Markdown table of bench.py lines: python tools/bench_table.py DIR [configs...]
-(reads DIR/bench_<config>.json, the last JSON line of each)."""
+"""Markdown table of bench.py lines: python tools/bench_table.py DIR [PREFIX] [configs...]
+(reads DIR/<PREFIX><config>.json, PREFIX default "bench_", the last JSON line of each)."""
 import json
 import os
 import sys
@@ -13,12 +13,16 @@ def line(path):
 
 def main():
     d = sys.argv[1]
-    cfgs = sys.argv[2:] or ["c2", "c1", "c3", "c4", "c5", "c2f", "c3f"]
+    rest = sys.argv[2:]
+    prefix = "bench_"
+    if rest and not rest[0].startswith("c"):
+        prefix, rest = rest[0], rest[1:]
+    cfgs = rest or ["c2", "c1", "c3", "c4", "c5", "c2f", "c3f"]
     print("| config | samples/s | e2e samples/s (host output) | ESS/s | lock-step speed-up (R(m)) | "
           "roofline frac (8(d)) | issue frac | CPU port | clocks |")
     print("|---|---:|---:|---:|---:|---:|---:|---:|---|")
     for c in cfgs:
-        p = os.path.join(d, f"bench_{c}.json")
+        p = os.path.join(d, f"{prefix}{c}.json")
         if not os.path.exists(p):
             continue
         b = line(p)
