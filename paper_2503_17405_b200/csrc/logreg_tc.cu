@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const long long r0 = (long long)i * BN + half * COLS;
       const int valid = r0 + COLS <= N ? COLS : (int)(N > r0 ? N - r0 : 0);
 #ifndef FSMC_SP_POLY
-#define FSMC_SP_POLY 1
+#define FSMC_SP_POLY 0
 #endif
 #if FSMC_SP_POLY
       // two MUFU operations per element (ex2, rcp) instead of three: with
