@@ -177,7 +177,9 @@ static cudaError_t launch_drmh_draws(const Params& p, int num_sms, cudaStream_t 
 
 cudaError_t dispatch_drmh(int op, int g, int e, Params& p, const LaunchCtx& lc, cudaStream_t s,
                            uint64_t ps, long long off, const double* x0, double jit) {
-  const int kind = p.t.kind;
+  // the compile-time MoG kernels unroll FSMC_MOG_SPECIAL_MODES modes: more
+  // modes run on the run-time plugin switch
+  const int kind = (p.t.kind == FSMC_T_MOG && p.t.n_modes > FSMC_MOG_SPECIAL_MODES) ? -1 : p.t.kind;
   if (op == 6) return launch_drmh_draws(p, lc.num_sms, s);
   if (p.k.precision == 1 && !p.k.split_body) {   // fp32 throughput mode: the sampling runs only
 #define F(GG, EE, TK)                                                                \

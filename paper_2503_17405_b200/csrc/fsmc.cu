@@ -344,7 +344,8 @@ fsmc_status check_args(const fsmc_kernel* k, const fsmc_target* t, const fsmc_st
 // the fp32 throughput mode's compiled (family, lanes, elements, plugin) set
 bool f32_compiled(const fsmc_kernel* k, const fsmc_target* t, const GE& ge) {
   bool ok = false;
-#define D(GG, EE, TK) ok = ok || (k->family == FSMC_DRMH && !k->split_body && ge.g == GG && ge.e == EE && t->kind == TK);
+#define D(GG, EE, TK) ok = ok || (k->family == FSMC_DRMH && !k->split_body && ge.g == GG && ge.e == EE && t->kind == TK && \
+                                   (TK != FSMC_T_MOG || t->n_modes <= FSMC_MOG_SPECIAL_MODES));
   FSMC_DRMH_F32(D)
 #undef D
 #define N(GG, EE, TK) ok = ok || (k->family == FSMC_NUTS && ge.g == GG && ge.e == EE && t->kind == TK);

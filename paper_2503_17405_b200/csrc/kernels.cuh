@@ -200,6 +200,9 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run
 }
 
 // ------------------------------------------------------------ windowed
+#ifndef FSMC_WIN_NT
+#define FSMC_WIN_NT 1
+#endif
 // fsm_run_kernel over pre-drawn windows (fsmc_run_windowed): the chain's
 // draws at counters dbase .. dbase + window - 1 are in p.draws[j]; it ticks
 // while a tick's worst case (dim + 1 draws for DRMH) still fits.
@@ -229,9 +232,22 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_win
     F<G, E> f;
     f.load(p, j, grp);
     bool ok = true;
+    if constexpr (VAR == 1 && F<G, E>::FULLD && FSMC_WIN_NT) {
+      // DRMH, default bundled order: every tick is exactly one proposal of
+      // dim + 1 draws, so the window and the tick limit fix the tick count
+      const long long per = G * E + 1;
+      long long nt = (lim - (long long)(c.ctr - c.dbase)) / per + 1;
+      nt = nt < p.tick_limit - c.tick ? nt : p.tick_limit - c.tick;
+      const int left = (int)(n_stop - c.count < (1LL << 30) ? n_stop - c.count : (1LL << 30));
+      const int count0 = (int)c.count;
 #pragma unroll 1
-    while (c.count < n_stop && c.tick < p.tick_limit && (long long)(c.ctr - c.dbase) <= lim)
-      if (!tick<F<G, E>, G, E, TK, false, VAR>(p, c, f, sm, j, grp)) { ok = false; break; }
+      for (int t = 0; t < (int)nt && (int)c.count - count0 < left; t++)
+        if (!tick<F<G, E>, G, E, TK, false, VAR>(p, c, f, sm, j, grp)) { ok = false; break; }
+    } else {
+#pragma unroll 1
+      while (c.count < n_stop && c.tick < p.tick_limit && (long long)(c.ctr - c.dbase) <= lim)
+        if (!tick<F<G, E>, G, E, TK, false, VAR>(p, c, f, sm, j, grp)) { ok = false; break; }
+    }
     f.store(p, j, grp);
     if (grp.lane == 0) {
       core_store(c, p, j);
