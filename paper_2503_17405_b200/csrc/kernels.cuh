@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run
 
 // ------------------------------------------------------------ windowed
 #ifndef FSMC_WIN_NT
-#define FSMC_WIN_NT 1
+#define FSMC_WIN_NT 0
 #endif
 // fsm_run_kernel over pre-drawn windows (fsmc_run_windowed): the chain's
 // draws at counters dbase .. dbase + window - 1 are in p.draws[j]; it ticks
