@@ -996,7 +996,7 @@ static int init_all(run_ctx* ctx) {
 int or_run_fsm(const or_kernel* k, const or_target* t, int64_t m, uint64_t seed,
                int64_t chain_offset, const double* x0, double init_jitter, int64_t n,
                int32_t variant, const int32_t* order, int64_t tick_chunk,
-               int64_t tick_budget, int32_t nthreads, or_run_out* out) {
+               int64_t tick_budget, int32_t surplus, int32_t nthreads, or_run_out* out) {
   run_ctx ctx;
   ctx_setup(&ctx, k, t, m, seed, chain_offset, x0, init_jitter, n, out);
   ctx.variant = variant;
@@ -1028,6 +1028,10 @@ int or_run_fsm(const or_kernel* k, const or_target* t, int64_t m, uint64_t seed,
   /* surplus ticks: finished chains keep stepping until the global stop or
    * the first failure, whichever comes first (lockstep.py:617-664) */
   int64_t run_to = tick_count < first_err ? tick_count : first_err;
+  /* surplus = 0 (the CPU baseline beside the device's surplus=False runs):
+   * the surplus ticks are skipped; only the aggregate counters change, and
+   * ticks up to a failure still run so it is reported as the reference does */
+  if (!surplus && first_err == INT64_MAX) run_to = INT64_MAX;
   if (run_to != INT64_MAX) run_jobs(&ctx, nthreads, 2, run_to, fsm_worker);
   /* first failure in (tick, chain) order (lockstep.py:648-649) */
   int64_t best_tick = INT64_MAX, best_j = -1;

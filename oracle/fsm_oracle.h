@@ -107,7 +107,7 @@ double or_log_density_grad(const or_target* t, const double* x, double* g);
 int or_run_fsm(const or_kernel* k, const or_target* t, int64_t m, uint64_t seed,
                int64_t chain_offset, const double* x0, double init_jitter, int64_t n,
                int32_t variant, const int32_t* order, int64_t tick_chunk,
-               int64_t tick_budget, int32_t nthreads, or_run_out* out);
+               int64_t tick_budget, int32_t surplus, int32_t nthreads, or_run_out* out);
 
 int or_run_standard(const or_kernel* k, const or_target* t, int64_t m, uint64_t seed,
                     int64_t chain_offset, const double* x0, double init_jitter, int64_t n,

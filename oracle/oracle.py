@@ -97,7 +97,8 @@ def lib():
                                     ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, _P,
                                     ctypes.c_double, ctypes.c_int64, ctypes.c_int32,
                                     ctypes.POINTER(ctypes.c_int32), ctypes.c_int64,
-                                    ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_Out)]
+                                    ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                    ctypes.POINTER(_Out)]
         _lib.or_run_standard.argtypes = [ctypes.POINTER(_Kernel), ctypes.POINTER(_Target),
                                          ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, _P,
                                          ctypes.c_double, ctypes.c_int64, ctypes.c_int32,
@@ -325,14 +326,18 @@ def _run(fn, kernel, target, m, n, seed, x0, init_jitter, chain_offset, nthreads
 
 
 def run_fsm(kernel, target, m, n, seed, variant="plain", order=None, tick_chunk=100,
-            tick_budget=None, x0=None, init_jitter=0.0, chain_offset=0, nthreads=1):
-    """lockstep.py:308-416 restated (two-phase stop; see fsm_oracle.c)."""
+            tick_budget=None, x0=None, init_jitter=0.0, chain_offset=0, nthreads=1,
+            surplus=True):
+    """lockstep.py:308-416 restated (two-phase stop; see fsm_oracle.c).
+    surplus=False skips the ticks chains take after their n-th sample (the
+    engine's surplus=False; samples and per-sample counts are unchanged)."""
     ordp = None
     if order is not None:
         oa = (ctypes.c_int32 * len(order))(*order)
         ordp = ctypes.cast(oa, ctypes.POINTER(ctypes.c_int32))
     return _run(lib().or_run_fsm, kernel, target, m, n, seed, x0, init_jitter, chain_offset,
-                nthreads, (VARIANTS[variant], ordp, int(tick_chunk), int(tick_budget or 0)))
+                nthreads, (VARIANTS[variant], ordp, int(tick_chunk), int(tick_budget or 0),
+                           int(bool(surplus))))
 
 
 def run_standard(kernel, target, m, n, seed, x0=None, init_jitter=0.0, chain_offset=0,

@@ -110,3 +110,21 @@ def test_oracle_threads_and_shards_are_exact():
     assert np.array_equal(np.concatenate([lo["samples"], hi["samples"]], axis=1), full["samples"])
     assert np.array_equal(np.concatenate([lo["sample_ticks"], hi["sample_ticks"]], axis=1),
                           full["sample_ticks"])
+
+
+def test_oracle_without_surplus_ticks_keeps_every_per_sample_field():
+    """run_fsm(surplus=False) (the CPU baseline beside the engine's
+    surplus=False bench runs) skips only the ticks chains take after their
+    n-th sample: samples, per-sample counts and tick_count are unchanged,
+    the aggregate block counts can only shrink."""
+    import numpy as np
+    from oracle import oracle as O
+    k, t = O.drmh(100, 0.1), O.mog(10, 0.9, [-3.0, 0.0, 3.0])
+    a = O.run_fsm(k, t, 24, 60, 5, variant="bundled", nthreads=4)
+    b = O.run_fsm(k, t, 24, 60, 5, variant="bundled", nthreads=4, surplus=False)
+    assert np.array_equal(a["samples"], b["samples"])
+    assert np.array_equal(a["iter_counts"], b["iter_counts"])
+    assert np.array_equal(a["sample_ticks"], b["sample_ticks"])
+    assert a["tick_count"] == b["tick_count"]
+    assert (b["block_exec_counts"] <= a["block_exec_counts"]).all()
+    assert (b["block_exec_counts"] < a["block_exec_counts"]).any()
