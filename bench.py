@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--no-lockstep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end legs (A/B runs)")
+    ap.add_argument("--one-device", action="store_true",
+                    help="tests: run every torchrun rank on cuda:0 with gloo collectives")
     ap.add_argument("--draw-window", type=int, default=-1,
                     help="DRMH pre-drawn window in draws (0: inline generator; -1: config default)")
     ap.add_argument("--draw-parts", type=int, default=0,
@@ -250,10 +252,20 @@ def main():
     import paper_2503_17405_b200 as fm
     from paper_2503_17405_b200 import analysis, distributed
 
+    if args.one_device:
+        # functional check of the multi-rank path on a one-GPU box: every rank
+        # on cuda:0, gloo collectives on host tensors (ranks never wait on one
+        # another inside a kernel); its timings say nothing about scaling
+        local = 0
     torch.cuda.set_device(local)
+    backend = "gloo" if args.one_device else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
 
     def barrier():
         if world > 1:
@@ -263,7 +275,7 @@ def main():
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -285,7 +297,9 @@ def main():
                                   prior_transform=cfg.get("prior_transform"),
                                   draw_parts=cfg.get("draw_parts", 1),
                                   prior_parts=cfg.get("prior_parts", 1),
-                                  precision=cfg.get("precision", "fp64"), _timing=timing)
+                                  precision=cfg.get("precision", "fp64"),
+                                  stop_sync=distributed.stop_sync() if world > 1 else None,
+                                  _timing=timing)
 
     held = None
     for s in range(args.warmup):
@@ -325,7 +339,7 @@ def main():
         if world > 1:
             loc = distributed.LocalMoments(mom.n, analysis_chain_means(samples, burn),
                                            mom.max_chain_var, mom.acov_tile, mom.acov_all)
-            mom = distributed.allreduce_moments(loc, device=dev)
+            mom = distributed.allreduce_moments(loc, device=coll_dev)
         ess = analysis.ess_from_moments(mom)
         ess_pooled = ess.pooled
         rhat_max = float(np.nanmax(analysis.rhat_from_moments(mom)))

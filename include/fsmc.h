@@ -54,7 +54,10 @@ enum {
   FSMC_T_FLAT = 8,           /* log density 0 */
   FSMC_T_LOGREG = 9,         /* Bayesian logistic regression, N(0, I) prior (BASELINE config 5) */
   FSMC_T_BOX = 10,           /* uniform on the box [a, b]^dim: 0 inside, -inf outside */
-  FSMC_T_GP_HYPER = 11       /* squared-exponential GP hyperparameters (sigma, tau, lam)  targets.py:191-265 */
+  FSMC_T_GP_HYPER = 11,      /* squared-exponential GP hyperparameters (sigma, tau, lam)  targets.py:191-265 */
+  FSMC_T_EXTERNAL = 12       /* no device plugin: every evaluation comes from the caller's batched
+                                evaluator (fsmc_advance / fsmc_init_deferred rounds); the
+                                per-chain entry points report FSMC_E_TARGET */
 };
 
 /* Gaussian-prior split for the elliptical kernel (targets.py:37-42) */

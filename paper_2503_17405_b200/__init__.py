@@ -15,7 +15,8 @@ from .lockstep import (ChainBatch, CostLedger, CostParams, KernelRunError, TickB
                        collect_samples, init_batch, measure_block_costs, run_fsm_batched,
                        run_standard_batched)
 from .prng import RngKey, key, normal, normal_vec, split, uniform, uniform_block
-from .targets import (GaussianPriorDecomposition, TargetError, TargetModel, conjugate_target,
+from .targets import (GaussianPriorDecomposition, TargetError, TargetModel, batched_target,
+                      conjugate_target,
                       correlated_mog_target, equicorrelated_covariance,
                       box_target, equicorrelated_gaussian_target, funnel_target, gaussian_target,
                       gp_classification_target, gp_hyperparameter_target,

@@ -24,7 +24,7 @@ MAX_MODES = 8
 DRMH, ESS, NUTS, SLICE = 1, 2, 3, 4
 PLAIN, BUNDLED, AMORTIZED = 0, 1, 2
 T_GAUSS_DIAG, T_GAUSS_DENSE, T_GAUSS_EQUICORR, T_MOG, T_FUNNEL, T_NANBAND, T_LOGISTIC, T_FLAT, \
-    T_LOGREG, T_BOX, T_GP_HYPER = range(1, 12)
+    T_LOGREG, T_BOX, T_GP_HYPER, T_EXTERNAL = range(1, 13)
 PRIOR_NONE, PRIOR_IDENTITY, PRIOR_DENSE = 0, 1, 2
 
 # per-chain int slots

@@ -7,9 +7,12 @@ constructors compute every constant with the same numpy/scipy calls as the
 reference (normalisers, inverse factors, precisions), so the per-evaluation
 arithmetic on the device starts from bit-identical inputs.
 
-Arbitrary Python callables are not accepted: there is no CPU fallback.
+A per-chain Python callable cannot run on the device (there is no CPU
+fallback); a user-defined target is written *batched* instead
+(:func:`batched_target`): a torch function of many chains' points at once,
+which the engine calls once per round in its batched-evaluation mode.
 ``log_density`` / ``gradient`` / ``log_density_and_grad`` evaluate through
-the device kernel (``fsmc_target_eval``) for API compatibility.
+the device kernel (``fsmc_target_eval``) or that function.
 """
 
 from __future__ import annotations
@@ -30,7 +33,7 @@ __all__ = [
     "correlated_mog_target", "funnel_target", "gp_classification_data",
     "gp_classification_target", "logistic_residual", "nan_band_target", "flat_target",
     "logistic_regression_data", "logistic_regression_target",
-    "conjugate_target",
+    "conjugate_target", "batched_target",
 ]
 
 _LOG_2PI = math.log(2.0 * math.pi)
@@ -448,3 +451,56 @@ def gp_classification_target(n_pts: int = 1024, seed: int = 20240617) -> TargetM
     residual -sum log(1 + exp(-y f))."""
     L, y = gp_classification_data(n_pts, seed)
     return _with_prior(logistic_residual(y), L, f"gpc-{n_pts}")
+
+
+def batched_target(name: str, dim: int, log_density=None, log_density_and_grad=None,
+                   gaussian_prior=None, log_density_cost: float = 1.0) -> TargetModel:
+    """A user-defined target, the plugin ``TargetModel(name, dim, log_density,
+    gradient, log_density_and_grad, gaussian_prior)`` (targets.py:45-60) in
+    batched form: every callable takes the points of many chains at once as a
+    float64 CUDA tensor ``theta [k, dim]`` and returns torch tensors --
+    ``log_density(theta) -> lp [k]``, ``log_density_and_grad(theta) -> (lp [k],
+    grad [k, dim])`` (needed by NUTS).  ``gaussian_prior=(chol, residual)``
+    (the elliptical kernel's split, targets.py:37-42) takes the prior factor
+    and the batched residual log density.
+
+    The engine runs such a target in its batched-evaluation mode: chains
+    advance on the device to their next log-density request, the requests of
+    a round are evaluated in one call of these functions, the chains resume;
+    starting points likewise (deferred init).  NaN / +inf results raise the
+    reference's BlockFailure as for the device plugins."""
+    if log_density is None and log_density_and_grad is None:
+        raise TargetError("batched_target needs log_density or log_density_and_grad")
+    dim = int(dim)
+
+    def full(theta, lp, g):
+        if g is not None:
+            if log_density_and_grad is None:
+                raise TargetError(f"target {name!r} has no gradient (log_density_and_grad)")
+            v, gr = log_density_and_grad(theta)
+            g.copy_(gr)
+        else:
+            v = log_density(theta) if log_density is not None else log_density_and_grad(theta)[0]
+        lp.copy_(v)
+
+    prior = None
+    residual = None
+    if gaussian_prior is not None:
+        chol, res_fn = gaussian_prior
+        residual = TargetModel(f"{name}-residual", dim, _lib.T_EXTERNAL, residual_only=True,
+                               has_gradient=False, log_density_cost=log_density_cost)
+
+        def res(theta, lp, g):
+            lp.copy_(res_fn(theta))
+        residual.batched_evaluator = lambda family=None: res
+        prior = GaussianPriorDecomposition(_check_chol(chol, "prior factor"), residual)
+    t = TargetModel(name, dim, _lib.T_EXTERNAL, gaussian_prior=prior,
+                    has_gradient=log_density_and_grad is not None,
+                    log_density_cost=log_density_cost)
+
+    def batched_evaluator(family=None):
+        if family == _lib.ESS and residual is not None:
+            return residual.batched_evaluator()
+        return full
+    t.batched_evaluator = batched_evaluator
+    return t
