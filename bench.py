@@ -207,8 +207,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--m", type=int, default=0, help="override chains per GPU")
-    ap.add_argument("--n", type=int, default=0, help="override samples per chain")
+    ap.add_argument("--m", "--chains", dest="m", type=int, default=0, help="override chains per GPU")
+    ap.add_argument("--n", "--samples", dest="n", type=int, default=0,
+                    help="override samples per chain")
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--no-lockstep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

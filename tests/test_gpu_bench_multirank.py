@@ -29,8 +29,8 @@ def _port():
 def test_bench_runs_two_ranks(config):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py",
-           "--gpus", "2", "--steps", "2", "--warmup", "1", "--config", config, "--m", "2048",
-           "--n", "60", "--no-cpu", "--one-device"]
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--config", config, "--chains", "2048",
+           "--samples", "60", "--no-cpu", "--one-device"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
