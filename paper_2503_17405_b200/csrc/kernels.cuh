@@ -206,8 +206,15 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run
 // fsm_run_kernel over pre-drawn windows (fsmc_run_windowed): the chain's
 // draws at counters dbase .. dbase + window - 1 are in p.draws[j]; it ticks
 // while a tick's worst case (dim + 1 draws for DRMH) still fits.
+#ifndef FSMC_WIN_MINB
+#define FSMC_WIN_MINB 0      // > 0: resident blocks the window kernels are compiled for
+#endif
+template <template <int, int> class F, int G, int E>
+__host__ __device__ constexpr int window_min_blocks() {
+  return FSMC_WIN_MINB > 0 ? FSMC_WIN_MINB : min_blocks_for<F, G, E>();
+}
 template <template <int, int> class F, int G, int E, int TK, int VAR = 0>
-__global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_window_kernel(Params p) {
+__global__ void __launch_bounds__(kThreads, (window_min_blocks<F, G, E>())) fsm_window_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
   // no cooperative-normal scratch: the draws are pre-generated, and the
