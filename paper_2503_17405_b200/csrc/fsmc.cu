@@ -690,8 +690,8 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->family != FSMC_DRMH) return fail(FSMC_ERR_UNSUPPORTED, "pre-drawn windows are for the DRMH kernels");
-  if (!draws || window < t->dim + 1 || window > 4096)
-    return fail(FSMC_ERR_ARG, "windowed run needs draws [m][window], dim + 1 <= window <= 4096");
+  if (!draws || window < t->dim + 1 || window > 65536)
+    return fail(FSMC_ERR_ARG, "windowed run needs draws [m][window], dim + 1 <= window <= 65536");
   if (n < 0) return fail(FSMC_ERR_ARG, "n must be >= 0");
   if (variant < FSMC_PLAIN || variant > FSMC_AMORTIZED) return fail(FSMC_ERR_ARG, "bad step variant");
   GE ge;
