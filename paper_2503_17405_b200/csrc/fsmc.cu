@@ -764,39 +764,65 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
     CUDA_TRY(cudaEventRecord(ev_fork, cs));
     for (int h = 1; h < parts; h++) CUDA_TRY(cudaStreamWaitEvent(sh[h], ev_fork, 0));
   }
-  const int kCheck = 4;   // rounds between reads of the unfinished counts
-  unsigned left[kMaxParts][2];   // per part: unfinished chains, lowest sample count of the last round
-  for (int h = 0; h < kMaxParts; h++) left[h][0] = 1;
+  // progress checks every kCheck rounds, read one check late: each check's
+  // counters go to pinned host memory asynchronously and are consumed at the
+  // next check, so the streams always hold queued rounds and never drain (a
+  // part seen finished stops receiving rounds; the <= kCheck rounds queued
+  // past its end find no unfinished chain and exit at once)
+  const int kCheck = 4;
+  unsigned* hc = nullptr;   // [2 checks][kMaxParts][unfinished, lowest count]
+  CUDA_TRY(cudaHostAlloc(&hc, 2 * kMaxParts * 2 * sizeof(unsigned), cudaHostAllocDefault));
+  cudaEvent_t evc[2][kMaxParts] = {};
+  for (int b = 0; b < 2; b++)
+    for (int h = 0; h < parts; h++) CUDA_TRY(cudaEventCreateWithFlags(&evc[b][h], cudaEventDisableTiming));
+  bool live[kMaxParts], asked[2][kMaxParts] = {};
+  for (int h = 0; h < kMaxParts; h++) live[h] = h < parts;
+  bool pending[2] = {false, false};
+  int cur = 0;
   for (long long r = 0;; r++) {
     for (int h = 0; h < parts; h++) {
-      if (!left[h][0]) continue;
+      if (!live[h]) continue;
       CUDA_TRY(dispatch_family(6, ge, ph[h], sh[h]));
       CUDA_TRY(cudaMemsetAsync(ph[h].next_chain, 0, sizeof(unsigned), sh[h]));
       CUDA_TRY(cudaMemsetAsync(ph[h].unfinished, 0, sizeof(unsigned), sh[h]));
       if (egress) CUDA_TRY(cudaMemsetAsync(ph[h].min_count, 0xff, sizeof(unsigned), sh[h]));
       CUDA_TRY(dispatch_family(5, ge, ph[h], sh[h]));
     }
-    if (r % kCheck == kCheck - 1) {
-      for (int h = 0; h < parts; h++)
-        if (left[h][0])
-          CUDA_TRY(cudaMemcpyAsync(left[h], ph[h].unfinished, (egress ? 2 : 1) * sizeof(unsigned),
-                                   cudaMemcpyDeviceToHost, sh[h]));
-      bool any = false;
-      for (int h = 0; h < parts; h++) {
-        CUDA_TRY(cudaStreamSynchronize(sh[h]));
-        any = any || left[h][0];
-      }
-      if (!any) break;
-      if (egress) {
-        // rows below every chain's sample count are final: a part that
-        // finished (or whose last round skipped every chain) bounds nothing
-        long long rows = n;
-        for (int h = 0; h < parts; h++)
-          if (left[h][0] && left[h][1] != 0xffffffffu) rows = std::min<long long>(rows, left[h][1]);
-        CUDA_TRY(send_rows(rows));
-      }
+    if (r % kCheck != kCheck - 1) continue;
+    for (int h = 0; h < parts; h++) {
+      asked[cur][h] = live[h];
+      if (!live[h]) continue;
+      CUDA_TRY(cudaMemcpyAsync(hc + (cur * kMaxParts + h) * 2, ph[h].unfinished,
+                               (egress ? 2 : 1) * sizeof(unsigned), cudaMemcpyDeviceToHost, sh[h]));
+      CUDA_TRY(cudaEventRecord(evc[cur][h], sh[h]));
     }
+    pending[cur] = true;
+    const int prev = cur ^ 1;
+    cur = prev;
+    if (!pending[prev]) continue;
+    pending[prev] = false;
+    bool any = false;
+    long long rows = n;
+    for (int h = 0; h < parts; h++) {
+      if (!asked[prev][h]) continue;
+      CUDA_TRY(cudaEventSynchronize(evc[prev][h]));
+      const unsigned* v = hc + (prev * kMaxParts + h) * 2;
+      if (!v[0]) live[h] = false;
+      any = any || v[0];
+      // rows below every chain's sample count are final: a part that
+      // finished (or whose last round skipped every chain) bounds nothing
+      if (egress && v[0] && v[1] != 0xffffffffu) rows = std::min<long long>(rows, v[1]);
+    }
+    if (!any) break;
+    if (egress) CUDA_TRY(send_rows(rows));
   }
+  // the unconsumed check still copies into hc: let it land before freeing
+  for (int b = 0; b < 2; b++)
+    for (int h = 0; h < parts; h++) {
+      if (pending[b] && asked[b][h]) CUDA_TRY(cudaEventSynchronize(evc[b][h]));
+      CUDA_TRY(cudaEventDestroy(evc[b][h]));
+    }
+  CUDA_TRY(cudaFreeHost(hc));
   if (egress) {
     CUDA_TRY(send_rows(n));
     CUDA_TRY(cudaEventCreateWithFlags(&ev_egress, cudaEventDisableTiming));
