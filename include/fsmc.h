@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define FSMC_ABI_VERSION 5
+#define FSMC_ABI_VERSION 6
 #define FSMC_WORK_WORDS 256 /* uint32 words of fsmc_state.work */
 #define FSMC_NINT 32        /* int64 slots per chain in fsmc_state.ints */
 #define FSMC_MAX_MODES 8    /* mixture components in FSMC_T_MOG */
@@ -132,7 +132,20 @@ typedef struct fsmc_outputs {
   double* samples;              /* [n][m][dim] or NULL */
   int32_t* loop_counts;         /* [L][n][m]: executions of each loop state per sample */
   int32_t* sample_ticks;        /* [n][m] tick that finished each sample, or NULL */
+  int64_t* loop_counts64;       /* [L][n][m] int64 (the reference's ledger type), used instead of
+                                   loop_counts when non-NULL, so the counts go to the host as is */
 } fsmc_outputs;
+
+/* Host destinations of a run's outputs (pinned host memory), filled while the
+ * run proceeds (fsmc_run_egress, fsmc_run_windowed_egress). */
+typedef struct fsmc_egress {
+  double* samples;              /* [n][m][dim] or NULL */
+  int64_t* loop_counts;         /* [L][n][m] or NULL (needs outputs.loop_counts64) */
+  int64_t* iter_counts;         /* [n][m] or NULL: a second copy of loop row `iter_loop`
+                                   (the ledger's iter_counts when one loop state counts) */
+  int32_t iter_loop;
+  int32_t n_loops;              /* L */
+} fsmc_egress;
 
 /* indices into fsmc_state.ints (per chain) */
 enum {
@@ -178,8 +191,8 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                      int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
                      const fsmc_outputs* out, int32_t lanes, void* stream_);
 
-/* fsmc_run with sample egress: `host_samples` (pinned host memory,
- * [n][m][dim], or NULL) receives out->samples.  With parts > 1 the chains run
+/* fsmc_run with output egress: `eg` (or NULL) names pinned host
+ * destinations for the samples and the ledger's count matrices.  With parts > 1 the chains run
  * in `parts` contiguous parts launched back to back on two streams (each
  * part's blocks backfill the SMs the previous part's tail frees) and every
  * finished part's sample columns are copied to the host (one pitched copy)
@@ -188,7 +201,7 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
  * independent).  The copies are ordered before later work on `stream`. */
 fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                             int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
-                            const fsmc_outputs* out, int32_t lanes, int32_t parts, double* host_samples,
+                            const fsmc_outputs* out, int32_t lanes, int32_t parts, const fsmc_egress* eg,
                             void* stream);
 
 /* Device -> host copy of `rows` rows of `width` bytes, both sides with row
@@ -239,8 +252,8 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
                                       int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
                                       int32_t lanes, int32_t parts, void* stream_);
 
-/* fsmc_run_windowed_overlap with sample egress: `host_samples` (pinned host
- * memory, [n][m][dim], or NULL) receives out->samples.  Rows every chain has
+/* fsmc_run_windowed_overlap with output egress: `eg` (or NULL) names pinned
+ * host destinations for the samples and the count matrices.  Rows every chain has
  * finished are copied on a device-owned egress stream while the later rows
  * are still being sampled (the windowed run reads each part's lowest sample
  * count at its periodic progress checks), so the device-to-host transfer
@@ -249,7 +262,7 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
 fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                                      int32_t variant, const int32_t* order, int64_t tick_limit,
                                      int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
-                                     int32_t lanes, int32_t parts, double* host_samples, void* stream);
+                                     int32_t lanes, int32_t parts, const fsmc_egress* eg, void* stream);
 
 /* Replaces measure_block_costs' timing loop (lockstep.py:454-498): runs every
  * chain with the plain executor up to tick_limit like fsmc_run (mode 1) and

@@ -15,7 +15,7 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FSMC_LIB", os.path.join(HERE, "libfsmc.so"))
 
-ABI_VERSION = 5    # fsmc.h FSMC_ABI_VERSION
+ABI_VERSION = 6    # fsmc.h FSMC_ABI_VERSION
 WORK_WORDS = 256   # fsmc.h FSMC_WORK_WORDS
 FSMC_NINT = 32
 MAX_MODES = 8
@@ -68,7 +68,12 @@ class State(ctypes.Structure):
 
 
 class Outputs(ctypes.Structure):
-    _fields_ = [("samples", _P), ("loop_counts", _P), ("sample_ticks", _P)]
+    _fields_ = [("samples", _P), ("loop_counts", _P), ("sample_ticks", _P), ("loop_counts64", _P)]
+
+
+class Egress(ctypes.Structure):
+    _fields_ = [("samples", _P), ("loop_counts", _P), ("iter_counts", _P), ("iter_loop", ctypes.c_int32),
+                ("n_loops", ctypes.c_int32)]
 
 
 _lib = None
@@ -105,7 +110,8 @@ def lib():
                            ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Outputs),
                            ctypes.c_int32, _P]
     L.fsmc_run_egress.restype = S
-    L.fsmc_run_egress.argtypes = list(L.fsmc_run.argtypes[:-1]) + [ctypes.c_int32, _P, _P]
+    L.fsmc_run_egress.argtypes = list(L.fsmc_run.argtypes[:-1]) + [ctypes.c_int32,
+                                                                   ctypes.POINTER(Egress), _P]
     L.fsmc_copy_to_host_2d.restype = S
     L.fsmc_copy_to_host_2d.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P]
     L.fsmc_advance.restype = S
@@ -161,7 +167,7 @@ def lib():
     L.fsmc_run_windowed_overlap.argtypes = list(L.fsmc_run_windowed.argtypes[:-1]) + [ctypes.c_int32, _P]
     L.fsmc_run_windowed_egress.restype = S
     L.fsmc_run_windowed_egress.argtypes = list(L.fsmc_run_windowed.argtypes[:-1]) + \
-        [ctypes.c_int32, _P, _P]
+        [ctypes.c_int32, ctypes.POINTER(Egress), _P]
     L.fsmc_profile_blocks.restype = S
     L.fsmc_profile_blocks.argtypes = [ctypes.POINTER(Kernel), ctypes.POINTER(Target),
                                       ctypes.POINTER(State), ctypes.c_int64, _P, _P]

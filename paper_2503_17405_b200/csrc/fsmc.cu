@@ -454,7 +454,7 @@ fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
 
 fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                             int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
-                            const fsmc_outputs* out, int32_t lanes, int32_t parts, double* host_samples,
+                            const fsmc_outputs* out, int32_t lanes, int32_t parts, const fsmc_egress* eg,
                             void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
@@ -482,13 +482,35 @@ fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_sta
   cudaStream_t cs = (cudaStream_t)stream_;
   p.j_lo = 0;
   p.j_hi = st->m;
-  if (!host_samples || !out || !out->samples || n <= 0 || parts <= 1 || st->m < 2 * parts) {
+  const bool any_egress = eg && out && n > 0 &&
+                          ((eg->samples && out->samples) || (out->loop_counts64 && (eg->loop_counts || eg->iter_counts)));
+  // the [lo, hi) chain columns of rows [0, n) of every output to the host
+  auto send_cols = [&](long long lo, long long hi, cudaStream_t es) -> cudaError_t {
+    cudaError_t e = cudaSuccess;
+    if (eg->samples && out->samples) {
+      const size_t row = (size_t)st->m * t->dim * sizeof(double), off = (size_t)lo * t->dim * sizeof(double);
+      e = cudaMemcpy2DAsync((char*)eg->samples + off, row, (const char*)out->samples + off, row,
+                            (size_t)(hi - lo) * t->dim * sizeof(double), (size_t)n, cudaMemcpyDeviceToHost, es);
+    }
+    if (e == cudaSuccess && out->loop_counts64) {
+      const size_t row = (size_t)st->m * sizeof(int64_t), off = (size_t)lo * sizeof(int64_t);
+      const size_t w = (size_t)(hi - lo) * sizeof(int64_t);
+      for (int l = 0; e == cudaSuccess && eg->loop_counts && l < eg->n_loops; l++)
+        e = cudaMemcpy2DAsync((char*)(eg->loop_counts + (size_t)l * n * st->m) + off, row,
+                              (const char*)(out->loop_counts64 + (size_t)l * n * st->m) + off, row, w, (size_t)n,
+                              cudaMemcpyDeviceToHost, es);
+      if (e == cudaSuccess && eg->iter_counts)
+        e = cudaMemcpy2DAsync((char*)eg->iter_counts + off, row,
+                              (const char*)(out->loop_counts64 + (size_t)eg->iter_loop * n * st->m) + off, row, w,
+                              (size_t)n, cudaMemcpyDeviceToHost, es);
+    }
+    return e;
+  };
+  if (!any_egress || parts <= 1 || st->m < 2 * parts) {
     p.next_chain = st->work;
     CUDA_TRY(cudaMemsetAsync(p.next_chain, 0, sizeof(unsigned), cs));
     CUDA_TRY(dispatch_family(1, ge, p, cs));
-    if (host_samples && out && out->samples && n > 0)
-      CUDA_TRY(cudaMemcpyAsync(host_samples, out->samples, (size_t)n * st->m * t->dim * sizeof(double),
-                               cudaMemcpyDeviceToHost, cs));
+    if (any_egress) CUDA_TRY(send_cols(0, st->m, cs));
     return FSMC_OK;
   }
   // chains in `parts` contiguous parts launched back to back on two alternating
@@ -506,7 +528,6 @@ fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_sta
   CUDA_TRY(cudaEventRecord(ev_fork, cs));
   CUDA_TRY(cudaStreamWaitEvent(side[1], ev_fork, 0));
   CUDA_TRY(cudaStreamWaitEvent(side[0], ev_fork, 0));
-  const size_t row = (size_t)st->m * t->dim * sizeof(double);
   for (int h = 0; h < parts; h++) {
     Params ph = p;
     ph.j_lo = st->m * h / parts;
@@ -517,10 +538,7 @@ fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_sta
     CUDA_TRY(dispatch_family(1, ge, ph, sh));
     CUDA_TRY(cudaEventRecord(ev_part[h], sh));
     CUDA_TRY(cudaStreamWaitEvent(side[0], ev_part[h], 0));
-    const size_t off = (size_t)ph.j_lo * t->dim * sizeof(double);
-    CUDA_TRY(cudaMemcpy2DAsync((char*)host_samples + off, row, (const char*)out->samples + off, row,
-                               (size_t)(ph.j_hi - ph.j_lo) * t->dim * sizeof(double), (size_t)n,
-                               cudaMemcpyDeviceToHost, side[0]));
+    CUDA_TRY(send_cols(ph.j_lo, ph.j_hi, side[0]));
   }
   CUDA_TRY(cudaEventRecord(ev_done, side[0]));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev_done, 0));   // the egress waited on every part
@@ -686,7 +704,7 @@ fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t
 fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                                      int32_t variant, const int32_t* order, int64_t tick_limit,
                                      int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
-                                     int32_t lanes, int32_t parts, double* host_samples, void* stream_) {
+                                     int32_t lanes, int32_t parts, const fsmc_egress* eg, void* stream_) {
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->family != FSMC_DRMH) return fail(FSMC_ERR_UNSUPPORTED, "pre-drawn windows are for the DRMH kernels");
@@ -724,7 +742,8 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   // fill the SMs another part's kernel tail and launch gaps leave idle
   // host_samples (pinned): rows every chain has finished are copied to the
   // host on the egress stream while later rows are still being sampled
-  const bool egress = host_samples && out && out->samples && n > 0;
+  const bool egress = eg && out && n > 0 &&
+                      ((eg->samples && out->samples) || (out->loop_counts64 && (eg->loop_counts || eg->iter_counts)));
   cudaStream_t side[kMaxParts] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxParts] = {}, ev_egress = nullptr;
   if (parts > 1 || egress) CUDA_TRY(side_streams(side));
@@ -733,13 +752,26 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
     for (int h = 1; h < parts; h++) CUDA_TRY(cudaEventCreateWithFlags(&ev_join[h], cudaEventDisableTiming));
   }
   const size_t row_bytes = (size_t)st->m * t->dim * sizeof(double);
+  const size_t crow = (size_t)st->m * sizeof(int64_t);
   long long rows_sent = 0;
   auto send_rows = [&](long long upto) -> cudaError_t {
     if (!egress || upto <= rows_sent) return cudaSuccess;
-    cudaError_t e = cudaMemcpyAsync((char*)host_samples + rows_sent * row_bytes,
-                                    (const char*)out->samples + rows_sent * row_bytes,
-                                    (size_t)(upto - rows_sent) * row_bytes, cudaMemcpyDeviceToHost, side[0]);
+    const long long a = rows_sent, nr = upto - rows_sent;
     rows_sent = upto;
+    cudaError_t e = cudaSuccess;
+    if (eg->samples && out->samples)
+      e = cudaMemcpyAsync((char*)eg->samples + a * row_bytes, (const char*)out->samples + a * row_bytes,
+                          (size_t)nr * row_bytes, cudaMemcpyDeviceToHost, side[0]);
+    if (out->loop_counts64) {
+      for (int l = 0; e == cudaSuccess && eg->loop_counts && l < eg->n_loops; l++)
+        e = cudaMemcpyAsync(eg->loop_counts + ((size_t)l * n + a) * st->m,
+                            out->loop_counts64 + ((size_t)l * n + a) * st->m, (size_t)nr * crow,
+                            cudaMemcpyDeviceToHost, side[0]);
+      if (e == cudaSuccess && eg->iter_counts)
+        e = cudaMemcpyAsync(eg->iter_counts + (size_t)a * st->m,
+                            out->loop_counts64 + ((size_t)eg->iter_loop * n + a) * st->m, (size_t)nr * crow,
+                            cudaMemcpyDeviceToHost, side[0]);
+    }
     return e;
   };
   static int draw_bps = -1;   // draws-kernel blocks per SM (FSMC_DRAW_BLOCKS_PER_SM; 0 = fill)

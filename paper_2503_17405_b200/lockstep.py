@@ -325,14 +325,19 @@ def _validate_run_args(batch: ChainBatch, n: int):
         raise ValueError("batch has already been run; build a fresh one")
 
 
-def _outputs(n, m, d, L, want_ticks, want_samples=True):
+def _outputs(n, m, d, L, want_ticks, want_samples=True, counts64=False):
+    """Device outputs; counts64: the loop counts in int64 (the reference's
+    ledger type) so they can go to the host without a conversion."""
     # every row < n of every chain is written by the kernel before it is read
     samples = torch.empty((n, m, d), dtype=torch.float64, device="cuda") if want_samples else None
-    loops = torch.empty((L, n, m), dtype=torch.int32, device="cuda")
+    loops = torch.empty((L, n, m), dtype=torch.int64 if counts64 else torch.int32, device="cuda")
     ticks = torch.empty((n, m), dtype=torch.int32, device="cuda") if want_ticks else None
     out = _lib.Outputs()
     out.samples = _lib.ptr(samples)
-    out.loop_counts = loops.data_ptr()
+    if counts64:
+        out.loop_counts64 = loops.data_ptr()
+    else:
+        out.loop_counts = loops.data_ptr()
     out.sample_ticks = _lib.ptr(ticks)
     return samples, loops, ticks, out
 
@@ -443,11 +448,27 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         validate_bundled_order(machine, order)
     m, d = batch.m, target.dim
     loop_states = bundle.loop_states
-    samples, loops, ticks_out, out = _outputs(n, m, d, len(loop_states), record_sample_ticks)
-    # output="numpy": the samples land in pinned host memory; the windowed
-    # DRMH run streams finished rows out while it samples (fsmc_run_windowed_egress)
-    host = _pinned((n, m, d), torch.float64) if output == "numpy" else None
+    to_host = output == "numpy"
+    samples, loops, ticks_out, out = _outputs(n, m, d, len(loop_states), record_sample_ticks,
+                                              counts64=to_host)
+    # output="numpy": the samples and the ledger's count matrices land in
+    # pinned host memory; the per-chain and windowed runs stream finished rows
+    # / chain parts out while they sample (fsmc_run_egress, fsmc_run_windowed_egress)
+    host = _pinned((n, m, d), torch.float64) if to_host else None
+    eg = None
+    host_counts = host_iter = None
+    if to_host:
+        host_counts = _pinned((len(loop_states), n, m), torch.int64)
+        eg = _lib.Egress()
+        eg.samples = host.data_ptr()
+        eg.loop_counts = host_counts.data_ptr()
+        eg.n_loops = len(loop_states)
+        if len(bundle.iter_states) == 1:
+            host_iter = _pinned((n, m), torch.int64)
+            eg.iter_counts = host_iter.data_ptr()
+            eg.iter_loop = loop_states.index(bundle.iter_states[0])
     egressed = False
+    counts_egressed = False
     limit = (tick_budget // tick_chunk) * tick_chunk if tick_budget is not None else _NO_LIMIT
     lib = _lib.lib()
     if precision not in ("fp64", "fp32"):
@@ -482,8 +503,8 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         draws = torch.empty(m * int(draw_window) + 32, dtype=torch.float64, device="cuda")
 
         def launch(mode, tick_limit):
-            nonlocal egressed
-            dst = host.data_ptr() if host is not None and mode == 0 else None
+            nonlocal egressed, counts_egressed
+            dst = ctypes.byref(eg) if eg is not None and mode == 0 else None
             _lib.check(lib.fsmc_run_windowed_egress(ctypes.byref(kern), ctypes.byref(tgt),
                                                     ctypes.byref(batch.struct()), n, variant, ordv,
                                                     tick_limit, mode, ctypes.byref(out),
@@ -491,18 +512,20 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
                                                     int(draw_parts), dst, _lib.stream_ptr()),
                        "fsmc_run_windowed_egress")
             egressed = egressed or dst is not None
+            counts_egressed = counts_egressed or dst is not None
     elif evaluator is None:
         def launch(mode, tick_limit):
-            nonlocal egressed
-            dst = host.data_ptr() if host is not None and mode == 0 else None
+            nonlocal egressed, counts_egressed
+            dst = ctypes.byref(eg) if eg is not None and mode == 0 else None
             # chains in parts of >= 2048 (about a resident wave): each finished
-            # part's samples stream to the host while the next parts run
+            # part's samples and counts stream to the host while the next parts run
             parts = max(1, min(8, m // 2048)) if dst else 1
             _lib.check(lib.fsmc_run_egress(ctypes.byref(kern), ctypes.byref(tgt),
                                            ctypes.byref(batch.struct()), n, variant, ordv, tick_limit,
                                            mode, ctypes.byref(out), lanes, parts, dst,
                                            _lib.stream_ptr()), "fsmc_run_egress")
             egressed = egressed or dst is not None
+            counts_egressed = counts_egressed or dst is not None
     else:
         launch = _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evaluator)
 
@@ -560,9 +583,10 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
             raise KernelRunError(chain=j, iteration=eiter, cause=_cause(bundle, kind, label))
     counts_now = info[:, 0]
     n_done = n if all_done else int(counts_now.min())
+    streamed = (host_counts, host_iter) if counts_egressed and n_done == n else None
     ledger = _fsm_ledger(bundle, params, step_variant, batch, loops, ticks_out, n_done,
                          tick_count if all_done else limit, walltime, output,
-                         native_shared=int(info[:, 6].sum()))
+                         native_shared=int(info[:, 6].sum()), streamed=streamed)
     if hasattr(launch, "stats"):
         ledger.extras.update(launch.stats)
     if not all_done:
@@ -741,18 +765,26 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
 
 
 def _fsm_ledger(bundle, params, variant, batch, loops, ticks_out, n_rows, ticks, walltime,
-                output, native_shared: int) -> CostLedger:
-    """lockstep.py:419-451"""
+                output, native_shared: int, streamed=None) -> CostLedger:
+    """lockstep.py:419-451.  ``streamed``: the count matrices already in
+    pinned host memory (int64 loop counts [L][n][m], iter_counts [n][m] or
+    None), copied there during the run."""
     K = bundle.fsm.n_states
     loop_states = bundle.loop_states
-    loop_execs = {s: _counts(loops[i, :n_rows], output) for i, s in enumerate(loop_states)}
+    if streamed is not None:
+        torch.cuda.current_stream().synchronize()
+        hc, hi = streamed
+        loop_execs = {s: hc[i].numpy() for i, s in enumerate(loop_states)}
+    else:
+        loop_execs = {s: _counts(loops[i, :n_rows], output) for i, s in enumerate(loop_states)}
     its = [loops[loop_states.index(s), :n_rows] for s in bundle.iter_states]
     it = its[0] if len(its) == 1 else sum(t.to(torch.int64) for t in its)
     blocks = batch.ints[:, _lib.I_BLOCKS:_lib.I_BLOCKS + K].sum(0)
     tc = params.tick_cost(variant)
     st = None if ticks_out is None else _counts(ticks_out[:n_rows], output)
     return CostLedger(
-        iter_counts=_counts(it, output),
+        iter_counts=streamed[1].numpy() if streamed is not None and streamed[1] is not None
+        else _counts(it, output),
         loop_exec_counts=loop_execs, tick_count=int(ticks),
         block_exec_counts=_convert(blocks, output), charged_cost=ticks * tc, walltime=walltime,
         regime=f"fsm-{variant}", tick_cost=tc,

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_entry_point():
     for s in syms:
         assert hasattr(lib, s), s
     lib.fsmc_abi_version.restype = ctypes.c_int32
-    assert lib.fsmc_abi_version() == 5   # fsmc.h FSMC_ABI_VERSION
+    assert lib.fsmc_abi_version() == 6   # fsmc.h FSMC_ABI_VERSION
 
 
 def test_state_without_work_words_is_rejected_before_any_launch():
