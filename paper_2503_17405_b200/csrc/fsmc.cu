@@ -801,7 +801,10 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   // next check, so the streams always hold queued rounds and never drain (a
   // part seen finished stops receiving rounds; the <= kCheck rounds queued
   // past its end find no unfinished chain and exit at once)
-  const int kCheck = 4;
+#ifndef FSMC_KCHECK
+#define FSMC_KCHECK 2
+#endif
+  const int kCheck = FSMC_KCHECK;   // rounds between progress checks
   unsigned* hc = nullptr;   // [2 checks][kMaxParts][unfinished, lowest count]
   CUDA_TRY(cudaHostAlloc(&hc, 2 * kMaxParts * 2 * sizeof(unsigned), cudaHostAllocDefault));
   cudaEvent_t evc[2][kMaxParts] = {};
