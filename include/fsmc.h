@@ -289,8 +289,10 @@ fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, d
  * evaluate, k = atomicAdd(req_count, 1).  The caller evaluates every listed
  * point in ONE batched call (e.g. GEMMs across chains), writes lp[k] (and
  * grad[k][:] for gradient kernels), and calls fsmc_advance again: each chain
- * first consumes its result, then runs on to its next request.  Repeat until
- * *req_count == 0.  Samples, ticks and ledger rows are identical to fsmc_run.
+ * first consumes its result (lp, grad; the point itself is kept in the
+ * chain's state, theta is write-only for the engine), then runs on to its
+ * next request.  Repeat until *req_count == 0.  Samples, ticks and ledger
+ * rows are identical to fsmc_run.
  * Buffers: theta/grad [m][dim], lp [m], req_chain [m] int32, req_count [1]. */
 fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                          int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
@@ -333,10 +335,13 @@ fsmc_status fsmc_advance_lockstep(const fsmc_kernel* k, const fsmc_target* t, fs
  * INIT block's nu = L eps (elliptical.py:73, prng.py:114-136 normal_vec with
  * chol) made one GEMM across chains.  Log densities are evaluated in place by
  * the plugin (as fsmc_run); every chain runs until its next INIT, draws eps,
- * and parks: req_chain[k] = j, nu[k][:] = eps, k = atomicAdd(req_count, 1).
- * The caller overwrites each row with L eps (e.g. nu[:k] = nu[:k] @ L^T in
- * one DGEMM, or fsmc_prior_apply below) and calls again; each chain resumes
- * INIT from its transformed row.  Repeat until *req_count == 0.  Samples,
+ * and parks in its own row: nu[j][:] = eps, req_chain[j] = j, and
+ * *req_count counts the parked chains.  The caller overwrites the rows with
+ * L eps (e.g. nu = nu @ L^T over all m rows in one DGEMM, or
+ * fsmc_prior_apply below; rows of chains that did not park are never read)
+ * and calls again; each chain resumes INIT from its transformed row.  (A
+ * compact row list would let a chain of the next round overwrite a row
+ * before its previous owner has read it.)  Repeat until *req_count == 0.  Samples,
  * ticks and ledger rows are those of fsmc_run (bit-identical with
  * fsmc_prior_apply; within the GEMM's rounding otherwise). */
 fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
@@ -346,7 +351,8 @@ fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_
 
 /* fsmc_advance_prior over the chains [j_lo, j_hi) only, with its own chain
  * queue (part 0..7): the chains split in parts whose rounds run on their own
- * streams, so one part's GEMM overlaps another part's advance kernel. */
+ * streams, so one part's GEMM overlaps another part's advance kernel.  nu and
+ * req_chain point at the part's first row: chain j parks in row j - j_lo. */
 fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                                     int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
                                     const fsmc_outputs* out, double* nu, int32_t* req_chain,

@@ -73,6 +73,9 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
 #ifndef FSMC_GEN_U
 #define FSMC_GEN_U 4
 #endif
+#ifndef FSMC_GEN_PIPE
+#define FSMC_GEN_PIPE 0
+#endif
 // register budget: ptxas's default for (256) threads (64 registers) measured
 // fastest; FSMC_GEN_MINB > 0 forces a minimum number of resident blocks
 #ifndef FSMC_GEN_MINB
@@ -103,12 +106,33 @@ __global__ void FSMC_GEN_BOUNDS drmh_draws_ilp_kernel(Params p) {
     int phase = (int)((ctr0 - (uint64_t)q[FSMC_I_DRAW0]) % (uint64_t)per) + lane % per;
     if (phase >= per) phase -= per;
     double* out = p.draws + (size_t)j * W;
+#if FSMC_GEN_PIPE
+    // software-pipelined: the next pass's integer hashes are computed in the
+    // same basic block as this pass's fp64 polynomials, so one warp's
+    // instruction stream mixes the integer and fp64 pipes
+    uint64_t hb[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) hb[u] = bits(hsc, ctr0 + (uint64_t)(32 * u + lane)) >> 11;
+#endif
     for (int c0 = 0; c0 < W; c0 += kDrawChunk) {
       const int c1 = min(W, c0 + kDrawChunk);
       int nt = 0;
       for (int k0 = c0; k0 < c1; k0 += 32 * U) {
         double bd[U], yr[U], vc[U];
         bool neg[U], cen[U], uni[U];
+#if FSMC_GEN_PIPE
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          bd[u] = (double)hb[u];
+          uni[u] = phase == d;
+          phase += step;
+          phase = phase >= per ? phase - per : phase;
+        }
+        // next pass (k0 + 32U; past the window end the values are unused)
+#pragma unroll
+        for (int u = 0; u < U; u++)
+          hb[u] = bits(hsc, ctr0 + (uint64_t)(k0 + 32 * (U + u) + lane)) >> 11;
+#else
 #pragma unroll
         for (int u = 0; u < U; u++) {   // prng.py:58-81, 103-111
           bd[u] = (double)(bits(hsc, ctr0 + (uint64_t)(k0 + 32 * u + lane)) >> 11);
@@ -116,6 +140,7 @@ __global__ void FSMC_GEN_BOUNDS drmh_draws_ilp_kernel(Params p) {
           phase += step;
           phase = phase >= per ? phase - per : phase;
         }
+#endif
 #pragma unroll
         for (int u = 0; u < U; u++) cen[u] = ndtri_classify((bd[u] + 0.5) * INV_2_53, &yr[u], &neg[u]);
 #pragma unroll

@@ -750,8 +750,11 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
                         continue
                     stats["rounds"] += 1
                     stats["prior_transforms"] += k
-                    lo = bounds[h][0]
-                    transform[h](nu[lo:lo + k])
+                    # each parked chain's eps is in its own row (j - lo): the
+                    # part's whole row range (rows of chains that did not
+                    # park are transformed and never read)
+                    lo, hi = bounds[h]
+                    transform[h](nu[lo:hi])
                     advance(h, mode, tick_limit)
                     still.append(h)
             active = still

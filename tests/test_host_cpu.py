@@ -73,6 +73,26 @@ HOST_HARNESS = r"""
 extern "C" double h_log(double x) { return fsmc::gl_log(x); }
 extern "C" double h_ndtri(double x) { return fsmc::ndtri(x); }
 extern "C" double h_softplus(double a) { return fsmc::softplus_neg(a); }
+extern "C" double h_exp(double x) { return fsmc::gl_exp(x); }
+extern "C" long h_exp_mismatch(long n, unsigned long long s) {
+  long bad = 0;
+  for (long t = 0; t < n; t++) {
+    s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+    const double v = (s >> 11) * 0x1p-53;
+    double x;
+    switch (t % 6) {
+      case 0: x = -v * 750.0; break;                    // accept tests, MoG modes
+      case 1: x = -708.0 - v * 40.0; break;             // subnormal results (special case)
+      case 2: x = v * 712.0; break;                     // overflow side
+      case 3: x = (v - 0.5) * 1e-15; break;             // tiny |x|
+      case 4: x = -745.1332191019411 - v * 0.1; break;  // underflow boundary
+      default: { unsigned long long u = s; std::memcpy(&x, &u, 8); }
+    }
+    double a = std::exp(x), b = fsmc::gl_exp(x);
+    if (std::memcmp(&a, &b, 8) != 0 && !(std::isnan(a) && std::isnan(b))) bad++;
+  }
+  return bad;
+}
 extern "C" double h_normal(unsigned long long seed, unsigned long long stream,
                            unsigned long long ctr) {
   return fsmc::normal(fsmc::hash_seed_stream(seed, stream), ctr);
@@ -106,13 +126,15 @@ def host_math(tmp_path_factory):
     subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-mfma", "-std=c++17", "-fPIC",
                            "-shared", f"-I{csrc}", "-o", str(so), str(src)])
     h = ctypes.CDLL(str(so))
-    for f in ("h_log", "h_ndtri", "h_softplus"):
+    for f in ("h_log", "h_ndtri", "h_softplus", "h_exp"):
         getattr(h, f).restype = ctypes.c_double
         getattr(h, f).argtypes = [ctypes.c_double]
     h.h_normal.restype = ctypes.c_double
     h.h_normal.argtypes = [ctypes.c_ulonglong] * 3
     h.h_log_mismatch.restype = ctypes.c_long
     h.h_log_mismatch.argtypes = [ctypes.c_long, ctypes.c_ulonglong]
+    h.h_exp_mismatch.restype = ctypes.c_long
+    h.h_exp_mismatch.argtypes = [ctypes.c_long, ctypes.c_ulonglong]
     return h
 
 
@@ -144,6 +166,20 @@ def test_glibc_log_restatement_is_bit_exact(host_math):
     assert host_math.h_log_mismatch(2_000_000, 88172645463325252) == 0
     for x in (1.0, 0.5, 2.0, 1e-300, 5e-324, 0.9999999999, 1.0625):
         assert host_math.h_log(x) == math.log(x)
+
+
+def test_glibc_exp_restatement_is_bit_exact(host_math):
+    """gl_exp (dmath.cuh) is Python's math.exp bit for bit: the DRMH accept test
+    (drmh.py:58-59) and the NUTS exponentials (nuts.py:45, 172, 201)."""
+    assert host_math.h_exp_mismatch(3_000_000, 0x9E3779B97F4A7C15) == 0
+    for x in (0.0, -0.0, 1e-300, -1e-17, 1.0, -1.0, 709.782712893384, 709.7827128933841,
+              -708.3964185322641, -745.1332191019411, -745.1332191019412, -1e4, 1e4,
+              float("inf"), float("-inf")):
+        try:
+            ref = math.exp(x)
+        except OverflowError:   # Python raises where libm returns +inf
+            ref = math.inf
+        assert host_math.h_exp(x) == ref, x
 
 
 def test_ndtri_restatement_matches_scipy(host_math):
