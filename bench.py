@@ -218,8 +218,9 @@ def main():
                     help="tests: run every torchrun rank on cuda:0 with gloo collectives")
     ap.add_argument("--draw-window", type=int, default=-1,
                     help="DRMH pre-drawn window in draws (0: inline generator; -1: config default)")
-    ap.add_argument("--draw-parts", type=int, default=0,
-                    help="DRMH windows: 1 or 2 chain halves overlapped on two streams (0: config)")
+    ap.add_argument("--draw-parts", type=int, default=-1,
+                    help="DRMH windows: 1..8 chain parts overlapped on their own streams, 0 = "
+                         "pipelined windows (double-buffered draws), -1: config default")
     ap.add_argument("--prior-parts", type=int, default=0,
                     help="ESS batched prior: chain parts overlapped on their own streams (0: config)")
     ap.add_argument("--prior", default="", choices=["", "none", "dmma", "trmm", "gemm", "device"],
@@ -234,7 +235,7 @@ def main():
         cfg["draw_window"] = args.draw_window
     if not args.lanes and cfg.get("lanes"):
         args.lanes = cfg["lanes"]     # e.g. C1: 128 chains, a whole block per chain
-    if args.draw_parts:
+    if args.draw_parts >= 0:
         cfg["draw_parts"] = args.draw_parts
     if args.prior_parts:
         cfg["prior_parts"] = args.prior_parts

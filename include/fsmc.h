@@ -359,6 +359,11 @@ fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, 
                                     int32_t* req_count, int32_t lanes, int64_t j_lo, int64_t j_hi,
                                     int32_t part, void* stream_);
 
+/* Device math for tests: out[i] = f(x[i]) on the device, f = 0 CUDA's exp,
+ * 1 exp_c (its constant-bank restatement), 2 gl_exp (glibc's exp restated),
+ * 3 gl_log (glibc's log restated), 4 CUDA's log. */
+fsmc_status fsmc_dmath_eval(int32_t fn, const double* x, int64_t n, double* out, void* stream_);
+
 /* nu[r][:] = L nu[r][:] in place for r < k (L = the target's dense prior
  * factor), each row summed in the sampling kernel's order: the bit-exact
  * prior transform for fsmc_advance_prior. */

@@ -112,6 +112,8 @@ def lib():
     L.fsmc_run_egress.restype = S
     L.fsmc_run_egress.argtypes = list(L.fsmc_run.argtypes[:-1]) + [ctypes.c_int32,
                                                                    ctypes.POINTER(Egress), _P]
+    L.fsmc_dmath_eval.restype = S
+    L.fsmc_dmath_eval.argtypes = [ctypes.c_int32, _P, ctypes.c_int64, _P, _P]
     L.fsmc_copy_to_host_2d.restype = S
     L.fsmc_copy_to_host_2d.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P]
     L.fsmc_advance.restype = S

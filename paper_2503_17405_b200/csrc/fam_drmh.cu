@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(256) drmh_draws_kernel(Params p) {
     const int64_t* q = p.st.ints + (size_t)j * FSMC_NINT;
     if (q[FSMC_I_ERR_KIND] != FSMC_E_NONE || q[FSMC_I_COUNT] >= n_stop || q[FSMC_I_TICK] >= p.tick_limit)
       continue;
-    const uint64_t ctr0 = (uint64_t)q[FSMC_I_COUNTER];
+    // pipelined windows: the counter this window starts at is known up front
+    const uint64_t ctr0 = p.draw_base ? (uint64_t)p.draw_base[j] + (uint64_t)(p.draw_round * p.draw_stride)
+                                      : (uint64_t)q[FSMC_I_COUNTER];
     const uint64_t hsc = hash_seed_stream(p.st.seed, (uint64_t)q[FSMC_I_STREAM]);
     int phase = (int)((ctr0 - (uint64_t)q[FSMC_I_DRAW0]) % (uint64_t)per) + lane % per;
     if (phase >= per) phase -= per;
@@ -101,7 +103,9 @@ __global__ void FSMC_GEN_BOUNDS drmh_draws_ilp_kernel(Params p) {
     const int64_t* q = p.st.ints + (size_t)j * FSMC_NINT;
     if (q[FSMC_I_ERR_KIND] != FSMC_E_NONE || q[FSMC_I_COUNT] >= n_stop || q[FSMC_I_TICK] >= p.tick_limit)
       continue;
-    const uint64_t ctr0 = (uint64_t)q[FSMC_I_COUNTER];
+    // pipelined windows: the counter this window starts at is known up front
+    const uint64_t ctr0 = p.draw_base ? (uint64_t)p.draw_base[j] + (uint64_t)(p.draw_round * p.draw_stride)
+                                      : (uint64_t)q[FSMC_I_COUNTER];
     const uint64_t hsc = hash_seed_stream(p.st.seed, (uint64_t)q[FSMC_I_STREAM]);
     int phase = (int)((ctr0 - (uint64_t)q[FSMC_I_DRAW0]) % (uint64_t)per) + lane % per;
     if (phase >= per) phase -= per;

@@ -670,6 +670,32 @@ __global__ void __launch_bounds__(256) prior_apply_kernel(const double* __restri
   }
 }
 
+// device math for tests: the restated functions against the library ones
+__global__ void dmath_eval_kernel(int fn, const double* __restrict__ x, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    double r;
+    switch (fn) {
+      case 0: r = exp(v); break;
+      case 1: r = exp_c(v); break;
+      case 2: r = gl_exp(v); break;
+      case 3: r = gl_log(v); break;
+      default: r = log(v); break;
+    }
+    out[i] = r;
+  }
+}
+
+fsmc_status fsmc_dmath_eval(int32_t fn, const double* x, int64_t n, double* out, void* stream_) {
+  if (!x || !out || n < 0 || fn < 0 || fn > 4) return fail(FSMC_ERR_ARG, "dmath_eval: fn in 0..4, x, out");
+  if (n == 0) return FSMC_OK;
+  fsmc::count_launch();
+  dmath_eval_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream_>>>(
+      fn, x, (long long)n, out);
+  CUDA_TRY(cudaGetLastError());
+  return FSMC_OK;
+}
+
 fsmc_status fsmc_prior_apply(const fsmc_target* t, double* nu, int64_t k, void* stream_) {
   if (!t || !nu || k < 0) return fail(FSMC_ERR_ARG, "prior_apply needs a target and nu");
   if (t->prior_kind != FSMC_PRIOR_DENSE || !t->prior_t)
@@ -733,7 +759,11 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   }
   p.draws = draws;
   p.window = window;
-  if (parts < 1 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 1..8");
+  if (parts < 0 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 0..8");
+  const bool pipelined = parts == 0;
+  if (pipelined && k->split_body)   // a split proposal can end a window between its draws
+    return fail(FSMC_ERR_UNSUPPORTED, "pipelined windows need the one-block DRMH proposal (split_body = 0)");
+  if (pipelined) parts = 1;
   if (st->m < parts) parts = 1;
   cudaStream_t cs = (cudaStream_t)stream_;
   unsigned* w = st->work;
@@ -780,6 +810,118 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
     draw_bps = e ? atoi(e) : 0;
     if (draw_bps < 0) draw_bps = 0;
   }
+  static int win_bps = -1;   // window-kernel blocks per SM (FSMC_WIN_BLOCKS_PER_SM; 0 = occupancy)
+  if (win_bps < 0) {
+    const char* e = getenv("FSMC_WIN_BLOCKS_PER_SM");
+    win_bps = e ? atoi(e) : 0;
+    if (win_bps < 0) win_bps = 0;
+  }
+#ifndef FSMC_KCHECK
+#define FSMC_KCHECK 2
+#endif
+  if (pipelined) {
+    // Pipelined windows: one chain range, draws double-buffered ([2][m][window]).
+    // Every window runs each unfinished chain exactly window / (dim + 1)
+    // proposals (a DRMH proposal takes dim normals and one uniform; the run
+    // stops a window right after the proposal that no longer leaves room for
+    // another), so window r + 1 of chain j starts at a counter known before
+    // window r runs: base_j + (r + 1) * stride.  The generator fills window
+    // r + 1 on its own stream while window r runs; a chain that finishes
+    // early simply never reads its later windows.
+    const long long per = t->dim + 1;
+    const long long stride = (window / per) * per;
+    long long* base = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&base, (size_t)st->m * sizeof(long long), cs));
+    CUDA_TRY(cudaMemcpy2DAsync(base, sizeof(long long), st->ints + FSMC_I_COUNTER, FSMC_NINT * sizeof(int64_t),
+                               sizeof(long long), (size_t)st->m, cudaMemcpyDeviceToDevice, cs));
+    if (!egress) CUDA_TRY(side_streams(side));
+    cudaStream_t gs = side[1];
+    Params pw = p;
+    pw.j_lo = 0;
+    pw.j_hi = st->m;
+    pw.next_chain = w;
+    pw.unfinished = w + 8;
+    pw.min_count = egress ? w + 9 : nullptr;
+    pw.draw_blocks_per_sm = draw_bps;
+    pw.win_blocks_per_sm = win_bps;
+    pw.draw_base = base;
+    pw.draw_stride = stride;
+    Params pg = pw;
+    double* buf[2] = {draws, draws + (size_t)st->m * window};
+    cudaEvent_t eg[2], ew[2], ev_start, ev_gen_done;
+    for (int b = 0; b < 2; b++) {
+      CUDA_TRY(cudaEventCreateWithFlags(&eg[b], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&ew[b], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_gen_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev_start, cs));
+    CUDA_TRY(cudaStreamWaitEvent(gs, ev_start, 0));
+    pg.draws = buf[0];
+    pg.draw_round = 0;
+    CUDA_TRY(dispatch_family(6, ge, pg, gs));
+    CUDA_TRY(cudaEventRecord(eg[0], gs));
+    const int kCheck = FSMC_KCHECK;
+    unsigned* hc = nullptr;   // [2 checks][unfinished, lowest count]
+    CUDA_TRY(cudaHostAlloc(&hc, 4 * sizeof(unsigned), cudaHostAllocDefault));
+    cudaEvent_t evc[2];
+    for (int b = 0; b < 2; b++) CUDA_TRY(cudaEventCreateWithFlags(&evc[b], cudaEventDisableTiming));
+    bool pending[2] = {false, false};
+    int cur = 0;
+    for (long long r = 0;; r++) {
+      const int b = (int)(r & 1);
+      pg.draws = buf[b ^ 1];   // the next window, into the half window r - 1 used
+      pg.draw_round = r + 1;
+      if (r >= 1) CUDA_TRY(cudaStreamWaitEvent(gs, ew[b ^ 1], 0));
+      CUDA_TRY(dispatch_family(6, ge, pg, gs));
+      CUDA_TRY(cudaEventRecord(eg[b ^ 1], gs));
+      CUDA_TRY(cudaStreamWaitEvent(cs, eg[b], 0));
+      CUDA_TRY(cudaMemsetAsync(pw.next_chain, 0, sizeof(unsigned), cs));
+      CUDA_TRY(cudaMemsetAsync(pw.unfinished, 0, sizeof(unsigned), cs));
+      if (egress) CUDA_TRY(cudaMemsetAsync(pw.min_count, 0xff, sizeof(unsigned), cs));
+      pw.draws = buf[b];
+      pw.draw_round = r;
+      CUDA_TRY(dispatch_family(5, ge, pw, cs));
+      CUDA_TRY(cudaEventRecord(ew[b], cs));
+      if (r % kCheck != kCheck - 1) continue;
+      // progress, read one check late (as the parts loop below)
+      CUDA_TRY(cudaMemcpyAsync(hc + cur * 2, pw.unfinished, (egress ? 2 : 1) * sizeof(unsigned),
+                               cudaMemcpyDeviceToHost, cs));
+      CUDA_TRY(cudaEventRecord(evc[cur], cs));
+      pending[cur] = true;
+      const int prev = cur ^ 1;
+      cur = prev;
+      if (!pending[prev]) continue;
+      pending[prev] = false;
+      CUDA_TRY(cudaEventSynchronize(evc[prev]));
+      const unsigned* v = hc + prev * 2;
+      if (!v[0]) break;
+      if (egress && v[1] != 0xffffffffu) CUDA_TRY(send_rows(std::min<long long>(n, v[1])));
+    }
+    for (int b = 0; b < 2; b++) {
+      if (pending[b]) CUDA_TRY(cudaEventSynchronize(evc[b]));
+      CUDA_TRY(cudaEventDestroy(evc[b]));
+    }
+    CUDA_TRY(cudaFreeHost(hc));
+    // the generator stream's last (unused) window joins the run's stream
+    CUDA_TRY(cudaEventRecord(ev_gen_done, gs));
+    CUDA_TRY(cudaStreamWaitEvent(cs, ev_gen_done, 0));
+    CUDA_TRY(cudaFreeAsync(base, cs));
+    if (egress) {
+      CUDA_TRY(send_rows(n));
+      CUDA_TRY(cudaEventCreateWithFlags(&ev_egress, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(ev_egress, side[0]));
+      CUDA_TRY(cudaStreamWaitEvent(cs, ev_egress, 0));
+      CUDA_TRY(cudaEventDestroy(ev_egress));
+    }
+    for (int b = 0; b < 2; b++) {
+      CUDA_TRY(cudaEventDestroy(eg[b]));
+      CUDA_TRY(cudaEventDestroy(ew[b]));
+    }
+    CUDA_TRY(cudaEventDestroy(ev_start));
+    CUDA_TRY(cudaEventDestroy(ev_gen_done));
+    return FSMC_OK;
+  }
   Params ph[kMaxParts];
   cudaStream_t sh[kMaxParts];
   for (int h = 0; h < parts; h++) {
@@ -801,9 +943,6 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   // next check, so the streams always hold queued rounds and never drain (a
   // part seen finished stops receiving rounds; the <= kCheck rounds queued
   // past its end find no unfinished chain and exit at once)
-#ifndef FSMC_KCHECK
-#define FSMC_KCHECK 2
-#endif
   const int kCheck = FSMC_KCHECK;   // rounds between progress checks
   unsigned* hc = nullptr;   // [2 checks][kMaxParts][unfinished, lowest count]
   CUDA_TRY(cudaHostAlloc(&hc, 2 * kMaxParts * 2 * sizeof(unsigned), cudaHostAllocDefault));

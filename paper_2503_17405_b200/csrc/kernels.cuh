@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, (window_min_blocks<F, G, E>())) fsm_
     if (c.count >= n_stop || c.tick >= p.tick_limit) continue;
     c.dw = p.draws + (size_t)j * p.window;
     c.dbase = c.ctr;
+    FSMC_CHECK(!p.draw_base || c.ctr == (uint64_t)p.draw_base[j] + (uint64_t)(p.draw_round * p.draw_stride));
     c.dlim = p.window;
     F<G, E> f;
     f.load(p, j, grp);
@@ -477,13 +478,14 @@ struct Launch {
   // a persistent chain-queue kernel with as many blocks as are co-resident
   template <class KF>
   static cudaError_t persistent(KF* kern, const Params& p, const LaunchCtx& lc, cudaStream_t s,
-                                size_t sm_bytes = 0, long long chains = -1) {
+                                size_t sm_bytes = 0, long long chains = -1, int max_per_sm = 0) {
     const size_t sb = sm_bytes ? sm_bytes : smem(p);
     int occ = 0;
     cudaError_t e = allow_smem(kern, sb);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, sb);
     if (e != cudaSuccess) return e;
+    if (max_per_sm > 0 && occ > max_per_sm) occ = max_per_sm;
     if (occ < 1) occ = 1;
     if (chains < 0) chains = p.st.m;
     long long need = (chains + (kThreads / G) - 1) / (kThreads / G);
@@ -506,8 +508,9 @@ struct Launch {
   static cudaError_t window(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     const size_t sb = std::max<size_t>(8, (size_t)(kThreads / G) * group_doubles(p.t) * sizeof(double));
     if constexpr (TK != 0)
-      if (unrolled(p)) return persistent(fsm_window_kernel<F, G, E, TK, 1>, p, lc, s, sb, p.j_hi - p.j_lo);
-    return persistent(fsm_window_kernel<F, G, E, TK, 0>, p, lc, s, sb, p.j_hi - p.j_lo);
+      if (unrolled(p))
+        return persistent(fsm_window_kernel<F, G, E, TK, 1>, p, lc, s, sb, p.j_hi - p.j_lo, p.win_blocks_per_sm);
+    return persistent(fsm_window_kernel<F, G, E, TK, 0>, p, lc, s, sb, p.j_hi - p.j_lo, p.win_blocks_per_sm);
   }
   static cudaError_t advance(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
     return persistent(fsm_advance_kernel<F, G, E>, p, lc, s, 0, p.j_hi - p.j_lo);

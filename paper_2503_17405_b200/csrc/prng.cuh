@@ -16,9 +16,34 @@ constexpr uint64_t STREAM_SALT = 0xC2B2AE3D27D4EB4FULL;
 constexpr uint64_t COUNTER_SALT = 0x165667B19E3779F9ULL;
 constexpr double INV_2_53 = 1.0 / 9007199254740992.0;
 
+// x * c mod 2^64 in three 32-bit multiplies chained into the high word
+// (FSMC_MUL3; the compiler's own form adds the cross terms separately)
+#ifndef FSMC_MUL3
+#define FSMC_MUL3 0
+#endif
+FSMC_HD uint64_t mulc64(uint64_t x, uint64_t c) {
+#if defined(__CUDA_ARCH__) && FSMC_MUL3
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+  const uint32_t cl = (uint32_t)c, ch = (uint32_t)(c >> 32);
+  uint32_t rl, rh;
+  asm("{\n\t"
+      ".reg .u64 t;\n\t"
+      "mul.wide.u32 t, %2, %4;\n\t"
+      "mov.b64 {%0, %1}, t;\n\t"
+      "mad.lo.u32 %1, %2, %5, %1;\n\t"
+      "mad.lo.u32 %1, %3, %4, %1;\n\t"
+      "}"
+      : "=r"(rl), "=r"(rh)
+      : "r"(xl), "r"(xh), "r"(cl), "r"(ch));
+  return ((uint64_t)rh << 32) | rl;
+#else
+  return x * c;
+#endif
+}
+
 FSMC_HD uint64_t mix64(uint64_t x) {
-  x = (x ^ (x >> 30)) * MIX_A;
-  x = (x ^ (x >> 27)) * MIX_B;
+  x = mulc64(x ^ (x >> 30), MIX_A);
+  x = mulc64(x ^ (x >> 27), MIX_B);
   return x ^ (x >> 31);
 }
 

@@ -429,8 +429,11 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     ``draw_window`` (DRMH kernels): generate each chain's next ``draw_window``
     PRNG draws in a separate full-occupancy kernel and let the step kernel
     read them (``fsmc_run_windowed``); bit-identical to the inline draws.
-    ``draw_parts`` (1..4) splits the chains in parts whose generator and
-    step kernels overlap on their own streams (``fsmc_run_windowed_overlap``).
+    ``draw_parts`` (1..8) splits the chains in parts whose generator and
+    step kernels overlap on their own streams (``fsmc_run_windowed_overlap``);
+    ``draw_parts=0`` pipelines the windows instead: every window runs each
+    chain exactly ``draw_window // (dim + 1)`` proposals, so window r + 1 is
+    generated (double-buffered) while window r runs, all chains in one launch.
     """
     _validate_run_args(batch, n)
     bundle.check_target(target)
@@ -500,7 +503,9 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     elif draw_window:
         # [m][window] plus a line of slack: the step kernel prefetches the
         # next proposal's draws, which for the last chain may lie past its window
-        draws = torch.empty(m * int(draw_window) + 32, dtype=torch.float64, device="cuda")
+        # (draw_parts=0: two windows per chain, the double buffer)
+        nbuf = 2 if int(draw_parts) == 0 else 1
+        draws = torch.empty(nbuf * m * int(draw_window) + 32, dtype=torch.float64, device="cuda")
 
         def launch(mode, tick_limit):
             nonlocal egressed, counts_egressed
