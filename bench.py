@@ -45,7 +45,7 @@ ISSUE_PROFILE = "r04_c2_issue.json"
 CONFIGS = {
     "c2": dict(workload="C2: DRMH FSM, correlated MoG d=10 (rho=0.9, modes -3/0/3), M=100, "
                         "scale=0.1, bundled", family="drmh", m=65536, n=1000, d=10,
-               variant="bundled", m_cpu=256, draw_window=4070, draw_parts=4),
+               variant="bundled", m_cpu=256, draw_window=4070, draw_parts=8),
     "c1": dict(workload="C1: elliptical slice FSM, conjugate Gaussian-likelihood d=100, amortized",
                family="ess", m=128, n=1000, d=100, variant="amortized", m_cpu=32, lanes=128),
     "c3": dict(workload="C3: NUTS FSM, equicorrelated Gaussian d=100 rho=0.99, eps=0.05, depth 10",
@@ -58,7 +58,7 @@ CONFIGS = {
                          "modes -3/0/3), M=100, scale=0.1, bundled; fp32 state and arithmetic, "
                          "fp64 reference draws rounded once; distributional parity only",
                 family="drmh", m=65536, n=1000, d=10, variant="bundled", m_cpu=256,
-                draw_window=4070, draw_parts=4, precision="fp32"),
+                draw_window=4070, draw_parts=8, precision="fp32"),
     "c3f": dict(workload="C3 in the fp32 throughput mode: NUTS FSM, equicorrelated Gaussian d=100 "
                          "rho=0.99, eps=0.05, depth 10; fp32 state and arithmetic; distributional "
                          "parity only",

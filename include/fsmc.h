@@ -242,11 +242,16 @@ fsmc_status fsmc_run_windowed(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
                               const fsmc_outputs* out, int64_t window, double* draws, int32_t lanes,
                               void* stream_);
 
-/* fsmc_run_windowed with the chains in `parts` (1..8) contiguous parts, each
+/* fsmc_run_windowed with the chains in `parts` (1..16) contiguous parts, each
  * alternating its draw-generation and window kernels on its own stream
  * (internal streams, joined back to stream_ before returning), so the parts'
- * kernels fill each other's kernel tails and launch gaps.  Results are
- * identical for any parts. */
+ * kernels fill each other's kernel tails and launch gaps.  parts = 0:
+ * pipelined windows instead, one chain range with `draws` holding two windows
+ * per chain ([2][m][window]); window r + 1 is generated while window r runs
+ * (every window runs each unfinished chain exactly window / (dim + 1)
+ * proposals; split-body DRMH is rejected).  Results are identical for any
+ * parts.  FSMC_DRAW_BLOCKS_PER_SM / FSMC_WIN_BLOCKS_PER_SM (environment) cap
+ * the two kernels' grids per SM so that several parts' kernels co-reside. */
 fsmc_status fsmc_run_windowed_overlap(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                                       int32_t variant, const int32_t* order, int64_t tick_limit,
                                       int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,

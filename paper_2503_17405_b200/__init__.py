@@ -6,6 +6,16 @@ by hand-written sm_100a CUDA kernels (``libfsmc.so``, C ABI in
 ``include/fsmc.h``).  There is no CPU fallback.
 """
 
+import os as _os
+
+# The windowed DRMH run drives up to 16 chain-part streams plus a
+# device-to-host egress stream.  With CUDA's default of 8 hardware work
+# queues per device, streams share queues and an egress copy stalls the
+# kernels queued behind it on an unrelated part (measured on B200: C2 with
+# host output 220 ms -> 176 ms per step at 32 queues).  Read once, when the
+# process creates its CUDA context; an explicit setting is kept.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .fsm import (BlockFailure, FsmDefinition, FsmError, SharedComputation, StepOutcome,
                   amortized_step, bundled_step, compose_nested, compose_sequential,
                   compose_single_loop, step)

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <mutex>
 #include <string>
 
@@ -49,7 +50,7 @@ int num_sms() {
 // Side streams of the overlapped windowed run, created once per device.  The
 // launch bookkeeping (chain queues, barrier words) lives in each state
 // block's own fsmc_state.work, so nothing else is shared between calls.
-constexpr int kMaxParts = 8;
+constexpr int kMaxParts = 16;   // windowed-run chain parts (work words 16 per part)
 std::mutex g_side_mu;
 cudaError_t side_streams(cudaStream_t (&out)[kMaxParts]) {
   static cudaStream_t side[kMaxDevices][kMaxParts] = {};
@@ -759,7 +760,7 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   }
   p.draws = draws;
   p.window = window;
-  if (parts < 0 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 0..8");
+  if (parts < 0 || parts > kMaxParts) return fail(FSMC_ERR_ARG, "windowed run: parts must be in 0..16");
   const bool pipelined = parts == 0;
   if (pipelined && k->split_body)   // a split proposal can end a window between its draws
     return fail(FSMC_ERR_UNSUPPORTED, "pipelined windows need the one-block DRMH proposal (split_body = 0)");
@@ -801,6 +802,44 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
         e = cudaMemcpyAsync(eg->iter_counts + (size_t)a * st->m,
                             out->loop_counts64 + ((size_t)eg->iter_loop * n + a) * st->m, (size_t)nr * crow,
                             cudaMemcpyDeviceToHost, side[0]);
+    }
+    return e;
+  };
+  // per chain part: rows [part_sent[h], upto) of the part's chain columns
+  // (pitched copies), so a part's finished rows leave without waiting for the
+  // slowest chain of every other part
+  long long part_sent[kMaxParts] = {};
+  static int trace = -1;   // FSMC_EGRESS_TRACE=1: host time of every egress copy issued (stderr)
+  if (trace < 0) trace = getenv("FSMC_EGRESS_TRACE") ? 1 : 0;
+  static int nocopy = -1;  // FSMC_EGRESS_NOCOPY=1 (experiments): the egress bookkeeping without the copies
+  if (nocopy < 0) nocopy = getenv("FSMC_EGRESS_NOCOPY") ? 1 : 0;
+  const auto t_start = std::chrono::steady_clock::now();
+  double t_wait = 0.0, t_send = 0.0;   // host ms in progress-check waits / egress copy calls (trace)
+  auto send_part = [&](int h, long long lo, long long hi, long long upto) -> cudaError_t {
+    if (!egress || upto <= part_sent[h] || hi <= lo) return cudaSuccess;
+    if (trace)
+      fprintf(stderr, "egress %.3f ms part %d rows %lld..%lld\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(), h,
+              part_sent[h], upto);
+    const long long a = part_sent[h], nr = upto - part_sent[h];
+    part_sent[h] = upto;
+    const size_t d8 = (size_t)t->dim * sizeof(double);
+    cudaError_t e = cudaSuccess;
+    if (nocopy) return e;
+    if (eg->samples && out->samples)
+      e = cudaMemcpy2DAsync((char*)eg->samples + a * row_bytes + lo * d8, row_bytes,
+                            (const char*)out->samples + a * row_bytes + lo * d8, row_bytes,
+                            (size_t)(hi - lo) * d8, (size_t)nr, cudaMemcpyDeviceToHost, side[0]);
+    if (out->loop_counts64) {
+      const size_t w8 = (size_t)(hi - lo) * sizeof(int64_t);
+      for (int l = 0; e == cudaSuccess && eg->loop_counts && l < eg->n_loops; l++)
+        e = cudaMemcpy2DAsync(eg->loop_counts + ((size_t)l * n + a) * st->m + lo, crow,
+                              out->loop_counts64 + ((size_t)l * n + a) * st->m + lo, crow, w8, (size_t)nr,
+                              cudaMemcpyDeviceToHost, side[0]);
+      if (e == cudaSuccess && eg->iter_counts)
+        e = cudaMemcpy2DAsync(eg->iter_counts + (size_t)a * st->m + lo, crow,
+                              out->loop_counts64 + ((size_t)eg->iter_loop * n + a) * st->m + lo, crow, w8,
+                              (size_t)nr, cudaMemcpyDeviceToHost, side[0]);
     }
     return e;
   };
@@ -922,6 +961,12 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
     CUDA_TRY(cudaEventDestroy(ev_gen_done));
     return FSMC_OK;
   }
+  static int part_streams = -1;   // FSMC_PART_STREAMS: streams the chain parts share (1..15)
+  if (part_streams < 0) {
+    const char* e = getenv("FSMC_PART_STREAMS");
+    part_streams = e ? atoi(e) : kMaxParts - 1;
+    part_streams = std::max(1, std::min(part_streams, kMaxParts - 1));
+  }
   Params ph[kMaxParts];
   cudaStream_t sh[kMaxParts];
   for (int h = 0; h < parts; h++) {
@@ -932,7 +977,10 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
     ph[h].unfinished = w + 16 * h + 8;   // [8] unfinished chains, [9] lowest sample count seen
     ph[h].min_count = egress ? w + 16 * h + 9 : nullptr;
     ph[h].draw_blocks_per_sm = draw_bps;
-    sh[h] = h == 0 ? cs : side[h];
+    // parts share FSMC_PART_STREAMS streams round robin (default: one per
+    // part up to 15; parts on one stream run back to back -- measured slower)
+    const int hs = h % part_streams;
+    sh[h] = hs == 0 ? cs : side[hs];
   }
   if (parts > 1) {
     CUDA_TRY(cudaEventRecord(ev_fork, cs));
@@ -953,10 +1001,28 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   for (int h = 0; h < kMaxParts; h++) live[h] = h < parts;
   bool pending[2] = {false, false};
   int cur = 0;
+  // at most gen_slots draw-generation kernels in flight: generator k (in
+  // launch order over parts and rounds) starts after generator k - gen_slots
+  // has finished, so the full-occupancy generators do not crowd out the
+  // latency-bound window kernels of the other parts
+  // (measured on B200, C2 at 8 parts: 3.62e8 samples/s unbounded, 4.08e8
+  // with 2 slots; default parts / 4, FSMC_GEN_SLOTS overrides, 0 = unbounded)
+  static int gen_slots_env = -2;
+  if (gen_slots_env == -2) {
+    const char* e = getenv("FSMC_GEN_SLOTS");
+    gen_slots_env = e ? std::max(0, atoi(e)) : -1;
+  }
+  const int gen_slots = std::min(kMaxParts, gen_slots_env >= 0 ? gen_slots_env : (parts >= 4 ? parts / 4 : 0));
+  cudaEvent_t gen_ring[kMaxParts] = {};
+  for (int i = 0; i < gen_slots; i++) CUDA_TRY(cudaEventCreateWithFlags(&gen_ring[i], cudaEventDisableTiming));
+  long long gen_k = 0;
   for (long long r = 0;; r++) {
     for (int h = 0; h < parts; h++) {
       if (!live[h]) continue;
+      if (gen_slots > 0 && gen_k >= gen_slots) CUDA_TRY(cudaStreamWaitEvent(sh[h], gen_ring[gen_k % gen_slots], 0));
       CUDA_TRY(dispatch_family(6, ge, ph[h], sh[h]));
+      if (gen_slots > 0) CUDA_TRY(cudaEventRecord(gen_ring[gen_k % gen_slots], sh[h]));
+      gen_k++;
       CUDA_TRY(cudaMemsetAsync(ph[h].next_chain, 0, sizeof(unsigned), sh[h]));
       CUDA_TRY(cudaMemsetAsync(ph[h].unfinished, 0, sizeof(unsigned), sh[h]));
       if (egress) CUDA_TRY(cudaMemsetAsync(ph[h].min_count, 0xff, sizeof(unsigned), sh[h]));
@@ -976,19 +1042,24 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
     if (!pending[prev]) continue;
     pending[prev] = false;
     bool any = false;
-    long long rows = n;
     for (int h = 0; h < parts; h++) {
       if (!asked[prev][h]) continue;
+      auto tw0 = std::chrono::steady_clock::now();
       CUDA_TRY(cudaEventSynchronize(evc[prev][h]));
+      t_wait += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count();
       const unsigned* v = hc + (prev * kMaxParts + h) * 2;
       if (!v[0]) live[h] = false;
       any = any || v[0];
-      // rows below every chain's sample count are final: a part that
-      // finished (or whose last round skipped every chain) bounds nothing
-      if (egress && v[0] && v[1] != 0xffffffffu) rows = std::min<long long>(rows, v[1]);
+      // rows below every chain's sample count in the part are final (a part
+      // that finished, or whose last round skipped every chain, has all n)
+      if (egress) {
+        const long long rows = !v[0] ? n : (v[1] != 0xffffffffu ? std::min<long long>(n, v[1]) : 0);
+        auto ts0 = std::chrono::steady_clock::now();
+        CUDA_TRY(send_part(h, ph[h].j_lo, ph[h].j_hi, rows));
+        t_send += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count();
+      }
     }
     if (!any) break;
-    if (egress) CUDA_TRY(send_rows(rows));
   }
   // the unconsumed check still copies into hc: let it land before freeing
   for (int b = 0; b < 2; b++)
@@ -997,8 +1068,13 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
       CUDA_TRY(cudaEventDestroy(evc[b][h]));
     }
   CUDA_TRY(cudaFreeHost(hc));
+  for (int i = 0; i < gen_slots; i++) CUDA_TRY(cudaEventDestroy(gen_ring[i]));
+  if (trace)
+    fprintf(stderr, "windowed run: host %.3f ms, %.3f ms in check waits, %.3f ms in egress copy calls\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(),
+            t_wait, t_send);
   if (egress) {
-    CUDA_TRY(send_rows(n));
+    for (int h = 0; h < parts; h++) CUDA_TRY(send_part(h, ph[h].j_lo, ph[h].j_hi, n));
     CUDA_TRY(cudaEventCreateWithFlags(&ev_egress, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(ev_egress, side[0]));
     CUDA_TRY(cudaStreamWaitEvent(cs, ev_egress, 0));

@@ -429,7 +429,7 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
     ``draw_window`` (DRMH kernels): generate each chain's next ``draw_window``
     PRNG draws in a separate full-occupancy kernel and let the step kernel
     read them (``fsmc_run_windowed``); bit-identical to the inline draws.
-    ``draw_parts`` (1..8) splits the chains in parts whose generator and
+    ``draw_parts`` (1..16) splits the chains in parts whose generator and
     step kernels overlap on their own streams (``fsmc_run_windowed_overlap``);
     ``draw_parts=0`` pipelines the windows instead: every window runs each
     chain exactly ``draw_window // (dim + 1)`` proposals, so window r + 1 is

@@ -96,3 +96,22 @@ def test_streamed_host_output_of_the_prior_transform_rounds(fm):
                      np.asarray(led.iter_counts) if output == "numpy" else led.iter_counts.cpu().numpy()))
     assert np.array_equal(runs[0][0], runs[1][0])
     assert np.array_equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("parts", [1, 3, 12, 0])
+def test_streamed_host_output_of_windowed_runs(fm, parts):
+    """The windowed DRMH run (C2's path) copies each chain part's finished
+    sample and count rows to pinned host memory at its progress checks
+    (per-part pitched copies; one range in the pipelined mode); the host
+    result equals the device-resident run's."""
+    bundle, target = fm.drmh_kernel(100, 0.1), fm.correlated_mog_target(10, 0.9, [-3.0, 0.0, 3.0])
+    m, n = 6000, 40
+    runs = []
+    for output in ("numpy", "torch"):
+        s, led = fm.run_fsm_batched(bundle, target, fm.init_batch(bundle, target, m, 21), n,
+                                    step_variant="bundled", output=output, surplus=False,
+                                    draw_window=1100, draw_parts=parts)
+        to_np = (lambda v: np.asarray(v)) if output == "numpy" else (lambda v: v.cpu().numpy())
+        runs.append((to_np(s), to_np(led.iter_counts), to_np(led.loop_exec_counts[2])))
+    for x, y in zip(*runs):
+        assert np.array_equal(x, y)
