@@ -39,8 +39,8 @@ METRIC = "samples/sec & ESS/sec at m chains (1/2/4/8 B200); speed-up vs lock-ste
 # executed fp64 flops per DRMH proposal on the MoG d=10 target (ncu SASS op
 # counts, DFMA counted twice: generator 65.1 per draw x 11 + step kernel 260)
 FP64_FLOPS_PER_PROPOSAL = 976.0
-# ncu instruction counts of the C2 kernel pair (tools/gpujobs/r04_*.sh)
-ISSUE_PROFILE = "r04_c2_issue.json"
+# ncu instruction counts of the C2 kernel pair (tools/gpujobs/r05_w.sh)
+ISSUE_PROFILE = "r05_c2_issue.json"
 
 CONFIGS = {
     "c2": dict(workload="C2: DRMH FSM, correlated MoG d=10 (rho=0.9, modes -3/0/3), M=100, "
@@ -501,7 +501,7 @@ def main():
             % t["measured_bytes_per_chain_sample"]
     if cfg["family"] == "drmh" and proposals:
         # executed fp64 flops per DRMH proposal (DFMA = 2), from ncu SASS counts of
-        # this pair of kernels (profiles/r04_c2_issue.json when present); peak =
+        # this pair of kernels (profiles/r05_c2_issue.json when present); peak =
         # measured DFMA rate
         ip = os.path.join(ROOT, "profiles", ISSUE_PROFILE)
         fpp, fsrc = FP64_FLOPS_PER_PROPOSAL, "profiles/r01b_c2_ncu.md"

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define FSMC_ABI_VERSION 6
+#define FSMC_ABI_VERSION 7   /* 7: prior-transform rows owned by chains, windowed parts 0..16, fsmc_dmath_eval */
 #define FSMC_WORK_WORDS 256 /* uint32 words of fsmc_state.work */
 #define FSMC_NINT 32        /* int64 slots per chain in fsmc_state.ints */
 #define FSMC_MAX_MODES 8    /* mixture components in FSMC_T_MOG */

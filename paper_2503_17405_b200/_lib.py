@@ -15,7 +15,7 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FSMC_LIB", os.path.join(HERE, "libfsmc.so"))
 
-ABI_VERSION = 6    # fsmc.h FSMC_ABI_VERSION
+ABI_VERSION = 7    # fsmc.h FSMC_ABI_VERSION
 WORK_WORDS = 256   # fsmc.h FSMC_WORK_WORDS
 FSMC_NINT = 32
 MAX_MODES = 8

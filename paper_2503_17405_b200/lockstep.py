@@ -730,37 +730,56 @@ def _prior_launcher(target, batch, n, variant, ordv, out, lanes, transform, part
                    "fsmc_copy_to_host_2d")
         sent[h] = upto
 
+    # one pinned completion word per part and round parity: a part's rounds are
+    # issued without waiting for the host, and its parked-chain count is read
+    # one round late (at most one extra, empty round per part at the end)
+    counts_h = torch.zeros((parts, 2), dtype=torch.int32, pin_memory=True)
+    done_ev = [[torch.cuda.Event() for _ in range(2)] for _ in range(parts)]
+
+    def issue(h, mode, tick_limit, r):
+        """round r of part h on its stream: (transform, when r > 0) + advance,
+        then its parked-chain count to pinned memory"""
+        lo, hi = bounds[h]
+        if r > 0:
+            transform[h](nu[lo:hi])
+        advance(h, mode, tick_limit)
+        counts_h[h, r & 1].copy_(req_count[h], non_blocking=True)
+        done_ev[h][r & 1].record()
+
     def launch(mode, tick_limit):
         for s in streams[1:]:
             s.wait_stream(main)
         if egress is not None:
             egress.wait_stream(main)
         sent = [0] * parts
-        done = [0] * parts           # advance calls completed per part
+        rounds = [0] * parts         # rounds issued per part
         active = list(range(parts))
         for h in active:
             with torch.cuda.stream(streams[h]):
-                advance(h, mode, tick_limit)
+                issue(h, mode, tick_limit, 0)
+                rounds[h] = 1
         while active:
             still = []
             for h in active:
                 with torch.cuda.stream(streams[h]):
-                    k = int(req_count[h].item())     # this part's advance has finished
-                    if mode == 0:
-                        send(h, min(done[h], n), sent)
-                    done[h] += 1
+                    r = rounds[h]
+                    # round r (transform of round r-1's parks + advance) goes
+                    # out before round r-1's count is read
+                    issue(h, mode, tick_limit, r)
+                    rounds[h] = r + 1
+                    done_ev[h][(r - 1) & 1].synchronize()
+                    k = int(counts_h[h, (r - 1) & 1])
+                    if mode == 0 and egress is not None:
+                        # after round r-1 (the part's r-th advance) rows [0, r-1) are final
+                        egress.wait_event(done_ev[h][(r - 1) & 1])
+                        send(h, min(r - 1, n), sent)
                     if k == 0:
-                        if mode == 0:
+                        if mode == 0 and egress is not None:
+                            egress.wait_stream(streams[h])
                             send(h, n, sent)
                         continue
                     stats["rounds"] += 1
                     stats["prior_transforms"] += k
-                    # each parked chain's eps is in its own row (j - lo): the
-                    # part's whole row range (rows of chains that did not
-                    # park are transformed and never read)
-                    lo, hi = bounds[h]
-                    transform[h](nu[lo:hi])
-                    advance(h, mode, tick_limit)
                     still.append(h)
             active = still
         for s in streams[1:]:

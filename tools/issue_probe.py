@@ -52,8 +52,8 @@ def summarise(csv_path, probe_path):
                  a.get("sm__sass_thread_inst_executed_op_dmul_pred_on.sum", 0.0) +
                  2 * a.get("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", 0.0)) / probe["proposals"]
     out = {"what": "warp instructions executed per DRMH proposal (C2: MoG d=10, m=65536, "
-                   "windowed draws in 4 parts), ncu sm__inst_executed.sum over every launch of "
-                   "the profiled run / its proposals",
+                   f"windowed draws in {probe.get('draw_parts', 4)} parts), ncu sm__inst_executed.sum over "
+                   "every launch of the profiled run / its proposals",
            "probe": probe, "launches": dict(launches),
            "warp_inst_per_proposal_by_kernel": per,
            "warp_inst_per_proposal": sum(per.values()),
