@@ -366,7 +366,8 @@ fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, 
 
 /* Device math for tests: out[i] = f(x[i]) on the device, f = 0 CUDA's exp,
  * 1 exp_c (its constant-bank restatement), 2 gl_exp (glibc's exp restated),
- * 3 gl_log (glibc's log restated), 4 CUDA's log. */
+ * 3 gl_log (glibc's log restated), 4 CUDA's log, 5 / 6 CUDA's sin / cos,
+ * 7 / 8 the sin / cos halves of CUDA's sincos. */
 fsmc_status fsmc_dmath_eval(int32_t fn, const double* x, int64_t n, double* out, void* stream_);
 
 /* nu[r][:] = L nu[r][:] in place for r < k (L = the target's dense prior

@@ -193,13 +193,130 @@ __global__ void FSMC_GEN_BOUNDS drmh_draws_ilp_kernel(Params p) {
   }
 }
 
+// The window fill with the central branch compacted as well: U slots per lane
+// per pass are hashed and classified; uniforms are stored at once, central
+// and tail items go to two per-warp queues.  The central queue is a 256-entry
+// ring carried across chunks and drained 32U items at a time (U polynomials
+// per lane, straight-line), so no lane evaluates a polynomial whose result it
+// discards (a uniform or a tail slot: a third of the slots); the remainder is
+// drained once at the window's end.  Bit-identical to the kernels above.
+#ifndef FSMC_GEN_CQ
+#define FSMC_GEN_CQ 0
+#endif
+template <int U>
+__global__ void FSMC_GEN_BOUNDS drmh_draws_cq_kernel(Params p) {
+  static_assert(32 * U <= 128, "ring holds at most 127 carried + 32U new items");
+  __shared__ double qy_all[8][kDrawChunk];
+  __shared__ unsigned qk_all[8][kDrawChunk];
+  __shared__ double cy_all[8][256];
+  __shared__ unsigned ck_all[8][256];
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = (int)p.window, d = p.t.dim, per = d + 1;
+  double* qy = qy_all[wid];
+  unsigned* qk = qk_all[wid];
+  double* cy = cy_all[wid];
+  unsigned* ck = ck_all[wid];
+  const unsigned lt = (1u << lane) - 1u;
+  const int step = 32 % per;
+  const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
+  for (long long j = p.j_lo + (long long)blockIdx.x * nw + wid; j < p.j_hi; j += (long long)gridDim.x * nw) {
+    const int64_t* q = p.st.ints + (size_t)j * FSMC_NINT;
+    if (q[FSMC_I_ERR_KIND] != FSMC_E_NONE || q[FSMC_I_COUNT] >= n_stop || q[FSMC_I_TICK] >= p.tick_limit)
+      continue;
+    const uint64_t ctr0 = p.draw_base ? (uint64_t)p.draw_base[j] + (uint64_t)(p.draw_round * p.draw_stride)
+                                      : (uint64_t)q[FSMC_I_COUNTER];
+    const uint64_t hsc = hash_seed_stream(p.st.seed, (uint64_t)q[FSMC_I_STREAM]);
+    int phase = (int)((ctr0 - (uint64_t)q[FSMC_I_DRAW0]) % (uint64_t)per) + lane % per;
+    if (phase >= per) phase -= per;
+    double* out = p.draws + (size_t)j * W;
+    unsigned chead = 0, ctail = 0;   // central ring [chead, ctail) (mod 256)
+    // U central polynomials per lane from the ring head; `all`: a partial
+    // batch (lanes past the tail compute on a dummy and store nothing)
+    auto drain = [&](bool all) {
+      double yv[U], rv[U];
+      unsigned kv[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const unsigned t = chead + (unsigned)(32 * u + lane);
+        const bool has = !all || t < ctail;
+        yv[u] = has ? cy[t & 255u] : 0.75;
+        kv[u] = has ? ck[t & 255u] : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) rv[u] = ndtri_central_sl(yv[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (kv[u] != 0xffffffffu) {
+          FSMC_CHECK((int)kv[u] < W);
+          out[kv[u]] = rv[u];
+        }
+      chead = all ? ctail : chead + 32u * U;
+    };
+    for (int c0 = 0; c0 < W; c0 += kDrawChunk) {
+      const int c1 = min(W, c0 + kDrawChunk);
+      int nt = 0;
+      for (int k0 = c0; k0 < c1; k0 += 32 * U) {
+        double bd[U], yr[U];
+        bool neg[U], cen[U], uni[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {   // prng.py:58-81, 103-111
+          bd[u] = (double)(bits(hsc, ctr0 + (uint64_t)(k0 + 32 * u + lane)) >> 11);
+          uni[u] = phase == d;
+          phase += step;
+          phase = phase >= per ? phase - per : phase;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) cen[u] = ndtri_classify((bd[u] + 0.5) * INV_2_53, &yr[u], &neg[u]);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int k = k0 + 32 * u + lane;
+          const bool live = k < c1;
+          if (live && uni[u]) out[k] = bd[u] * INV_2_53;       // prng.py:97-100
+          const bool cn = live && !uni[u] && cen[u];
+          const bool tl = live && !uni[u] && !cen[u];
+          const unsigned bc = __ballot_sync(0xffffffffu, cn);
+          const unsigned bt = __ballot_sync(0xffffffffu, tl);
+          if (cn) {
+            const unsigned pos = (ctail + __popc(bc & lt)) & 255u;
+            cy[pos] = yr[u];
+            ck[pos] = (unsigned)k;
+          }
+          if (tl) {
+            const int pos = nt + __popc(bt & lt);
+            qy[pos] = yr[u];
+            qk[pos] = (unsigned)k | (neg[u] ? 0x80000000u : 0u);
+          }
+          ctail += __popc(bc);
+          nt += __popc(bt);
+        }
+        __syncwarp();
+        if (ctail - chead >= 32u * U) {
+          drain(false);
+          __syncwarp();
+        }
+      }
+      for (int t = lane; t < nt; t += 32) {
+        const unsigned kk = qk[t];
+        FSMC_CHECK((int)(kk & 0x7fffffffu) < W && nt <= kDrawChunk);
+        out[kk & 0x7fffffffu] = ndtri_tail_sl(qy[t], (kk >> 31) != 0);
+      }
+      __syncwarp();
+    }
+    while (ctail != chead) {   // the window's remainder
+      drain(true);
+      __syncwarp();
+    }
+  }
+}
+
 static cudaError_t launch_drmh_draws(const Params& p, int num_sms, cudaStream_t s) {
   const int threads = 256, nw = threads / 32;
   long long need = (p.j_hi - p.j_lo + nw - 1) / nw;
   const int per_sm = p.draw_blocks_per_sm > 0 ? p.draw_blocks_per_sm : 8;
   int blocks = (int)std::max<long long>(1, std::min<long long>(need, (long long)num_sms * per_sm));
   count_launch();
-  if (FSMC_GEN_U > 1) drmh_draws_ilp_kernel<FSMC_GEN_U><<<blocks, threads, 0, s>>>(p);
+  if (FSMC_GEN_CQ) drmh_draws_cq_kernel<FSMC_GEN_U><<<blocks, threads, 0, s>>>(p);
+  else if (FSMC_GEN_U > 1) drmh_draws_ilp_kernel<FSMC_GEN_U><<<blocks, threads, 0, s>>>(p);
   else drmh_draws_kernel<<<blocks, threads, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -681,14 +681,18 @@ __global__ void dmath_eval_kernel(int fn, const double* __restrict__ x, long lon
       case 1: r = exp_c(v); break;
       case 2: r = gl_exp(v); break;
       case 3: r = gl_log(v); break;
-      default: r = log(v); break;
+      case 4: r = log(v); break;
+      case 5: r = sin(v); break;
+      case 6: r = cos(v); break;
+      case 7: { double sv, cv; sincos(v, &sv, &cv); r = sv; break; }
+      default: { double sv, cv; sincos(v, &sv, &cv); r = cv; break; }
     }
     out[i] = r;
   }
 }
 
 fsmc_status fsmc_dmath_eval(int32_t fn, const double* x, int64_t n, double* out, void* stream_) {
-  if (!x || !out || n < 0 || fn < 0 || fn > 4) return fail(FSMC_ERR_ARG, "dmath_eval: fn in 0..4, x, out");
+  if (!x || !out || n < 0 || fn < 0 || fn > 8) return fail(FSMC_ERR_ARG, "dmath_eval: fn in 0..8, x, out");
   if (n == 0) return FSMC_OK;
   fsmc::count_launch();
   dmath_eval_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream_>>>(
