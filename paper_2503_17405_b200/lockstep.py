@@ -18,6 +18,7 @@ reference's types) or stay in HBM as torch tensors (``output="torch"``).
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Any, Sequence
@@ -522,9 +523,9 @@ def run_fsm_batched(bundle, target, batch: ChainBatch, n: int, step_variant: str
         def launch(mode, tick_limit):
             nonlocal egressed, counts_egressed
             dst = ctypes.byref(eg) if eg is not None and mode == 0 else None
-            # chains in parts of >= 2048 (about a resident wave): each finished
-            # part's samples and counts stream to the host while the next parts run
-            parts = max(1, min(8, m // 2048)) if dst else 1
+            # chains in parts: each finished part's samples and counts stream
+            # to the host while the next parts run
+            parts = max(1, min(_EGRESS_PARTS_MAX, m // _EGRESS_PART_CHAINS)) if dst else 1
             _lib.check(lib.fsmc_run_egress(ctypes.byref(kern), ctypes.byref(tgt),
                                            ctypes.byref(batch.struct()), n, variant, ordv, tick_limit,
                                            mode, ctypes.byref(out), lanes, parts, dst,
@@ -663,6 +664,12 @@ def _batched_launcher(bundle, target, batch, n, variant, ordv, out, lanes, evalu
 
 
 _SIDE_STREAMS: dict = {}      # per device, reused across runs (prior_parts)
+# per-chain runs with host output (fsmc_run_egress): chain parts of at least
+# this many chains, at most this many parts; each finished part's columns go
+# to the host while later parts run, so the copy left after the run is one
+# part's (C3 e2e: 5.40e7 at 8 parts of 2048 chains, 5.71e7 at 16 of 1024)
+_EGRESS_PART_CHAINS = int(os.environ.get("FSMC_EGRESS_PART_CHAINS", "1024"))
+_EGRESS_PARTS_MAX = int(os.environ.get("FSMC_EGRESS_PARTS_MAX", "16"))
 _EGRESS_STREAMS: dict = {}    # per device: device -> host sample copies
 
 
