@@ -33,6 +33,16 @@ template <int G, int E>
 __device__ __forceinline__ double* group_scratch(double* smem, int gd) {
   return smem + (kThreads / 32) * normal_scratch_doubles<E>() + (threadIdx.x / G) * gd;
 }
+// a family's vectors kept in the group's shared memory (FF::SVECS, the NUTS
+// trajectory ends) follow the plugin scratch in each group's region
+template <class FF, int G, int E>
+__host__ __device__ inline int group_doubles_f(const fsmc_target& t) {
+  return group_doubles(t) + FF::SVECS * G * E;
+}
+template <class FF, int G>
+__device__ __forceinline__ void bind_state(FF& f, double* sm, const fsmc_target& t, const Grp<G>& grp) {
+  if constexpr (FF::SVECS > 0) f.bind(sm + group_doubles(t), grp.lane);
+}
 template <int G, int E>
 inline size_t smem_bytes(int gd) {
   return ((size_t)(kThreads / G) * gd + (size_t)(kThreads / 32) * normal_scratch_doubles<E>()) *
@@ -56,6 +66,11 @@ __host__ __device__ constexpr int min_blocks() { return G == 1 ? 4 : (G == 32 ? 
 // resident blocks would spill its twelve-vector state
 // fp32 throughput-mode families (half the register footprint per vector):
 // more resident blocks
+// warp-per-chain families with vectors in shared memory (NUTS ends): fewer
+// registers, more resident blocks
+#ifndef FSMC_SMEM_WARP_MIN_BLOCKS
+#define FSMC_SMEM_WARP_MIN_BLOCKS 4
+#endif
 #ifndef FSMC_F32_MIN_BLOCKS
 #define FSMC_F32_MIN_BLOCKS 5          // thread-per-chain groups
 #endif
@@ -69,7 +84,8 @@ constexpr bool is_f32_family() {
 template <template <int, int> class F, int G, int E>
 __host__ __device__ constexpr int min_blocks_for() {
   return is_f32_family<F<G, E>>() ? (G == 1 ? FSMC_F32_MIN_BLOCKS : FSMC_F32_WARP_MIN_BLOCKS)
-                                  : ((G == 128 && F<G, E>::GRAD) ? 1 : min_blocks<G>());
+                                  : ((G == 128 && F<G, E>::GRAD) ? 1
+                                     : ((G == 32 && F<G, E>::SVECS > 0) ? FSMC_SMEM_WARP_MIN_BLOCKS : min_blocks<G>()));
 }
 
 struct LaunchCtx {
@@ -84,10 +100,10 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
   extern __shared__ double smem[];
   Grp<G> grp;
   const int gib = threadIdx.x / G;
-  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
+  double* sm = group_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
   const long long groups = (long long)gridDim.x * (kThreads / G);
   const int d = p.t.dim;
-  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
+  double* ws = warp_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
   for (long long j = (long long)blockIdx.x * (kThreads / G) + gib; j < p.st.m; j += groups) {
     Core c;
     memset(&c, 0, sizeof(c));
@@ -96,6 +112,7 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
     c.hsc = hash_seed_stream(p.st.seed, stream);
     c.state = 1;
     F<G, E> f;
+    bind_state<F<G, E>, G>(f, sm, p.t, grp);
 #pragma unroll
     for (int e = 0; e < E; e++) {
       int i = grp.idx(e);
@@ -137,7 +154,9 @@ __global__ void __launch_bounds__(kThreads) fsm_init_kernel(Params p, uint64_t p
 // starting point (lp[j], j = chain), exactly as fsm_init_kernel would
 template <template <int, int> class F, int G, int E>
 __global__ void __launch_bounds__(kThreads) fsm_init_finish_kernel(Params p) {
+  extern __shared__ double smem[];
   Grp<G> grp;
+  double* sm = group_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
   const int gib = threadIdx.x / G;
   const long long groups = (long long)gridDim.x * (kThreads / G);
   for (long long j = (long long)blockIdx.x * (kThreads / G) + gib; j < p.st.m; j += groups) {
@@ -145,6 +164,7 @@ __global__ void __launch_bounds__(kThreads) fsm_init_finish_kernel(Params p) {
     core_load(c, p, j);
     if (c.err_kind != FSMC_E_NONE) continue;
     F<G, E> f;
+    bind_state<F<G, E>, G>(f, sm, p.t, grp);
     f.load(p, j, grp);
     bool ok = true;
     if constexpr (F<G, E>::SHAPE != SHAPE_NESTED) {
@@ -173,8 +193,8 @@ template <template <int, int> class F, int G, int E, int TK, int VAR = 0>
 __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
-  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
+  double* sm = group_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
+  double* ws = warp_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
   while (true) {   // chains [j_lo, j_hi) of the state block (fsmc_run_egress runs it in parts)
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
@@ -185,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_run
     c.ws = ws;
     if (c.err_kind != FSMC_E_NONE) continue;
     F<G, E> f;
+    bind_state<F<G, E>, G>(f, sm, p.t, grp);
     f.load(p, j, grp);
     bool ok = true;
     const long long n_stop = p.mode == 0 ? p.n : (1LL << 62);
@@ -238,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, (window_min_blocks<F, G, E>())) fsm_
     FSMC_CHECK(!p.draw_base || c.ctr == (uint64_t)p.draw_base[j] + (uint64_t)(p.draw_round * p.draw_stride));
     c.dlim = p.window;
     F<G, E> f;
+    bind_state<F<G, E>, G>(f, sm, p.t, grp);
     f.load(p, j, grp);
     bool ok = true;
     if constexpr (VAR == 1 && F<G, E>::FULLD && FSMC_WIN_NT) {
@@ -274,8 +296,8 @@ template <template <int, int> class F, int G, int E>
 __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_profile_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
-  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
+  double* sm = group_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
+  double* ws = warp_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
   while (true) {
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
@@ -286,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<G>()) fsm_profile_kernel(
     c.ws = ws;
     if (c.err_kind != FSMC_E_NONE) continue;
     F<G, E> f;
+    bind_state<F<G, E>, G>(f, sm, p.t, grp);
     f.load(p, j, grp);
     bool ok = true;
 #pragma unroll 1
@@ -306,8 +329,8 @@ template <template <int, int> class F, int G, int E, int TK = 0, bool INLINE = f
 __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_advance_kernel(Params p) {
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
-  double* ws = warp_scratch<G, E>(smem, group_doubles(p.t));
+  double* sm = group_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
+  double* ws = warp_scratch<G, E>(smem, group_doubles_f<F<G, E>, G, E>(p.t));
   while (true) {
     long long j = 0;
     if (grp.lane == 0) j = atomicAdd(p.next_chain, 1u);
@@ -318,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_for<F, G, E>())) fsm_adv
     c.ws = ws;
     if (c.err_kind != FSMC_E_NONE) continue;
     F<G, E> f;
+    bind_state<F<G, E>, G>(f, sm, p.t, grp);
     f.load(p, j, grp);
     long long resume = p.st.ints[(size_t)j * FSMC_NINT + FSMC_I_RESUME];
     bool ok = true;
@@ -381,15 +405,16 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
   using FF = F<G, E>;
   extern __shared__ double smem[];
   Grp<G> grp;
-  double* sm = group_scratch<G, E>(smem, group_doubles(p.t));
+  double* sm = group_scratch<G, E>(smem, group_doubles_f<FF, G, E>(p.t));
   const long long j = p.wave_lo + (long long)blockIdx.x * (kThreads / G) + threadIdx.x / G;
   bool live = j < p.wave_hi;
   Core c;
-  c.ws = warp_scratch<G, E>(smem, group_doubles(p.t));
+  c.ws = warp_scratch<G, E>(smem, group_doubles_f<FF, G, E>(p.t));
   FF f;
+  bind_state<FF, G>(f, sm, p.t, grp);
   if (live) {
     core_load(c, p, j);
-    c.ws = warp_scratch<G, E>(smem, group_doubles(p.t));
+    c.ws = warp_scratch<G, E>(smem, group_doubles_f<FF, G, E>(p.t));
     f.load(p, j, grp);
     live = c.err_kind == FSMC_E_NONE;
   }
@@ -457,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) lockstep_kernel(Params p) {
 // ------------------------------------------------------------- launchers
 template <template <int, int> class F, int G, int E, int TK>
 struct Launch {
-  static size_t smem(const Params& p) { return smem_bytes<G, E>(group_doubles(p.t)); }
+  static size_t smem(const Params& p) { return smem_bytes<G, E>(group_doubles_f<F<G, E>, G, E>(p.t)); }
   static cudaError_t init(const Params& p, uint64_t ps, long long off, const double* x0, double jit,
                           cudaStream_t s) {
     long long groups = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
@@ -472,7 +497,9 @@ struct Launch {
     long long groups = (p.st.m + (kThreads / G) - 1) / (kThreads / G);
     int blocks = (int)std::min<long long>(groups, 1 << 20);
     count_launch();
-    fsm_init_finish_kernel<F, G, E><<<blocks, kThreads, 0, s>>>(p);
+    cudaError_t ea = allow_smem(fsm_init_finish_kernel<F, G, E>, smem(p));
+    if (ea != cudaSuccess) return ea;
+    fsm_init_finish_kernel<F, G, E><<<blocks, kThreads, smem(p), s>>>(p);
     return cudaGetLastError();
   }
   // a persistent chain-queue kernel with as many blocks as are co-resident
