@@ -31,7 +31,9 @@ def test_library_exports_every_declared_entry_point():
     for s in syms:
         assert hasattr(lib, s), s
     lib.fsmc_abi_version.restype = ctypes.c_int32
-    assert lib.fsmc_abi_version() == 6   # fsmc.h FSMC_ABI_VERSION
+    hdr = open(os.path.join(ROOT, "include", "fsmc.h")).read()
+    abi = int(re.search(r"#define FSMC_ABI_VERSION (\d+)", hdr).group(1))
+    assert lib.fsmc_abi_version() == abi   # fsmc.h FSMC_ABI_VERSION
 
 
 def test_state_without_work_words_is_rejected_before_any_launch():
