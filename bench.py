@@ -129,12 +129,24 @@ class ClockSampler:
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        self.q, self.index = q, index
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
+        # sampling is live before the timed region starts (nvidia-smi takes a
+        # while to produce its first row)
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < 5.0:
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.01)
+        self.skip = 0
+        if self.p is not None:
+            with open(self.f.name) as g:
+                self.skip = len([r for r in g.read().splitlines() if r.strip()])
 
     def stop(self) -> dict:
         if self.p is None:
@@ -144,6 +156,15 @@ class ClockSampler:
         self.f.seek(0)
         rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
         os.unlink(self.f.name)
+        rows = rows[self.skip:]          # rows written before the timed region began
+        if not rows:                     # a region shorter than the interval: one row right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=20).stdout
+                rows = [r.split(", ") for r in out.strip().splitlines() if r.strip()]
+            except (OSError, subprocess.SubprocessError):
+                rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm, mx, reasons = [], None, set()
         for r in rows:
