@@ -20,6 +20,7 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "nvtx_range.h"
 
 using namespace fsmc;
 
@@ -393,6 +394,7 @@ fsmc_status fsmc_state_layout(const fsmc_kernel* k, int64_t dim, int32_t* n_vec,
 
 fsmc_status fsmc_prng_fill(uint64_t seed, uint64_t stream, uint64_t counter, int64_t count, int32_t kind,
                            void* out, void* stream_) {
+  FSMC_NVTX("fsmc_prng_fill");
   if (count < 0 || kind < 0 || kind > 2 || (!out && count)) return fail(FSMC_ERR_ARG, "bad prng_fill args");
   if (!count) return FSMC_OK;
   int blocks = (int)std::min<long long>((count + 255) / 256, 148LL * 16);
@@ -422,17 +424,20 @@ static fsmc_status init_common(const fsmc_kernel* k, const fsmc_target* t, fsmc_
 
 fsmc_status fsmc_init(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, uint64_t parent_stream,
                       int64_t chain_offset, const double* x0, double init_jitter, void* stream_) {
+  FSMC_NVTX("fsmc_init");
   return init_common(k, t, st, parent_stream, chain_offset, x0, init_jitter, stream_, false);
 }
 
 fsmc_status fsmc_init_deferred(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                                uint64_t parent_stream, int64_t chain_offset, const double* x0,
                                double init_jitter, void* stream_) {
+  FSMC_NVTX("fsmc_init_deferred");
   return init_common(k, t, st, parent_stream, chain_offset, x0, init_jitter, stream_, true);
 }
 
 fsmc_status fsmc_init_finish(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, const double* lp,
                              void* stream_) {
+  FSMC_NVTX("fsmc_init_finish");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (!lp) return fail(FSMC_ERR_ARG, "init_finish needs lp [m]");
@@ -450,6 +455,7 @@ fsmc_status fsmc_init_finish(const fsmc_kernel* k, const fsmc_target* t, fsmc_st
 fsmc_status fsmc_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n, int32_t variant,
                      const int32_t* order, int64_t tick_limit, int32_t mode, const fsmc_outputs* out,
                      int32_t lanes, void* stream_) {
+  FSMC_NVTX("fsmc_run");
   return fsmc_run_egress(k, t, st, n, variant, order, tick_limit, mode, out, lanes, 1, nullptr, stream_);
 }
 
@@ -457,6 +463,7 @@ fsmc_status fsmc_run_egress(const fsmc_kernel* k, const fsmc_target* t, fsmc_sta
                             int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
                             const fsmc_outputs* out, int32_t lanes, int32_t parts, const fsmc_egress* eg,
                             void* stream_) {
+  FSMC_NVTX("fsmc_run_egress");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (n < 0) return fail(FSMC_ERR_ARG, "n must be >= 0");
@@ -604,6 +611,7 @@ fsmc_status fsmc_advance(const fsmc_kernel* k, const fsmc_target* t, fsmc_state*
                          int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
                          const fsmc_outputs* out, const double* lp, const double* grad, double* theta,
                          int32_t* req_chain, int32_t* req_count, int32_t lanes, void* stream_) {
+  FSMC_NVTX("fsmc_advance");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
@@ -617,6 +625,7 @@ fsmc_status fsmc_advance_lockstep(const fsmc_kernel* k, const fsmc_target* t, fs
                                   const fsmc_outputs* out, const double* lp, const double* grad,
                                   double* theta, int32_t* req_chain, int32_t* req_count, int64_t* level,
                                   int32_t lanes, void* stream_) {
+  FSMC_NVTX("fsmc_advance_lockstep");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
@@ -630,6 +639,7 @@ fsmc_status fsmc_advance_prior(const fsmc_kernel* k, const fsmc_target* t, fsmc_
                                int32_t variant, const int32_t* order, int64_t tick_limit, int32_t mode,
                                const fsmc_outputs* out, double* nu, int32_t* req_chain,
                                int32_t* req_count, int32_t lanes, void* stream_) {
+  FSMC_NVTX("fsmc_advance_prior");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
@@ -646,6 +656,7 @@ fsmc_status fsmc_advance_prior_part(const fsmc_kernel* k, const fsmc_target* t, 
                                     const fsmc_outputs* out, double* nu, int32_t* req_chain,
                                     int32_t* req_count, int32_t lanes, int64_t j_lo, int64_t j_hi,
                                     int32_t part, void* stream_) {
+  FSMC_NVTX("fsmc_advance_prior_part");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
@@ -702,6 +713,7 @@ fsmc_status fsmc_dmath_eval(int32_t fn, const double* x, int64_t n, double* out,
 }
 
 fsmc_status fsmc_prior_apply(const fsmc_target* t, double* nu, int64_t k, void* stream_) {
+  FSMC_NVTX("fsmc_prior_apply");
   if (!t || !nu || k < 0) return fail(FSMC_ERR_ARG, "prior_apply needs a target and nu");
   if (t->prior_kind != FSMC_PRIOR_DENSE || !t->prior_t)
     return fail(FSMC_ERR_ARG, "prior_apply needs a dense prior factor");
@@ -736,6 +748,7 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
                                      int32_t variant, const int32_t* order, int64_t tick_limit,
                                      int32_t mode, const fsmc_outputs* out, int64_t window, double* draws,
                                      int32_t lanes, int32_t parts, const fsmc_egress* eg, void* stream_) {
+  FSMC_NVTX("fsmc_run_windowed_egress");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->family != FSMC_DRMH) return fail(FSMC_ERR_UNSUPPORTED, "pre-drawn windows are for the DRMH kernels");
@@ -912,6 +925,8 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
     bool pending[2] = {false, false};
     int cur = 0;
     for (long long r = 0;; r++) {
+    FSMC_NVTX("windowed round");
+      FSMC_NVTX("windowed round");
       const int b = (int)(r & 1);
       pg.draws = buf[b ^ 1];   // the next window, into the half window r - 1 used
       pg.draw_round = r + 1;
@@ -1021,6 +1036,7 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
   for (int i = 0; i < gen_slots; i++) CUDA_TRY(cudaEventCreateWithFlags(&gen_ring[i], cudaEventDisableTiming));
   long long gen_k = 0;
   for (long long r = 0;; r++) {
+    FSMC_NVTX("windowed round");
     for (int h = 0; h < parts; h++) {
       if (!live[h]) continue;
       if (gen_slots > 0 && gen_k >= gen_slots) CUDA_TRY(cudaStreamWaitEvent(sh[h], gen_ring[gen_k % gen_slots], 0));
@@ -1097,6 +1113,7 @@ fsmc_status fsmc_run_windowed_egress(const fsmc_kernel* k, const fsmc_target* t,
 
 fsmc_status fsmc_profile_blocks(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                                 int64_t tick_limit, unsigned long long* cycles, void* stream_) {
+  FSMC_NVTX("fsmc_profile_blocks");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
@@ -1124,6 +1141,7 @@ fsmc_status fsmc_profile_blocks(const fsmc_kernel* k, const fsmc_target* t, fsmc
 
 fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st, int64_t n,
                               const fsmc_outputs* out, int32_t lanes, void* stream_) {
+  FSMC_NVTX("fsmc_lockstep_run");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
@@ -1148,6 +1166,7 @@ fsmc_status fsmc_lockstep_run(const fsmc_kernel* k, const fsmc_target* t, fsmc_s
 
 fsmc_status fsmc_lockstep_barrier_probe(const fsmc_kernel* k, const fsmc_target* t, fsmc_state* st,
                                         int64_t iters, int32_t lanes, void* stream_) {
+  FSMC_NVTX("fsmc_lockstep_barrier_probe");
   fsmc_status s = check_args(k, t, st);
   if (s != FSMC_OK) return s;
   if (k->precision != 0) return fail(FSMC_ERR_UNSUPPORTED, "the fp32 throughput mode covers fsmc_run and the windowed DRMH runs");
@@ -1181,6 +1200,7 @@ fsmc_status fsmc_copy_to_host_2d(void* dst, const void* src, int64_t pitch, int6
 
 fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, double* lp, double* grad,
                              int32_t family, int32_t lanes, void* stream_) {
+  FSMC_NVTX("fsmc_target_eval");
   if (!t || !X || !lp || m < 0) return fail(FSMC_ERR_ARG, "bad target_eval args");
   if (!m) return FSMC_OK;
   GE ge;
@@ -1206,6 +1226,7 @@ fsmc_status fsmc_target_eval(const fsmc_target* t, const double* X, int64_t m, d
 
 fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, int64_t N, float* R,
                                  double* lp, void* stream_) {
+  FSMC_NVTX("fsmc_logreg_epilogue");
   if (!Z || !y || !R || !lp || rows < 0 || N < 1) return fail(FSMC_ERR_ARG, "bad epilogue args");
   if (!rows) return FSMC_OK;
   if (rows > 65535) return fail(FSMC_ERR_ARG, "at most 65535 rows per epilogue call");
@@ -1219,6 +1240,7 @@ fsmc_status fsmc_logreg_epilogue(const float* Z, const float* y, int64_t rows, i
 fsmc_status fsmc_diag_partials(const double* samples, int64_t n, int64_t m, int64_t dim, int64_t burn,
                                int64_t lag0, int64_t n_lags, double* chain_mean, double* acov,
                                double* chain_var, void* stream_) {
+  FSMC_NVTX("fsmc_diag_partials");
   if (!samples || n - burn < 2 || m < 1 || dim < 1 || !chain_mean) return fail(FSMC_ERR_ARG, "bad diag args");
   cudaStream_t cs = (cudaStream_t)stream_;
   if (lag0 == 0) {

@@ -25,6 +25,7 @@
 
 #include "../../include/fsmc.h"
 #include "launch_count.h"
+#include "nvtx_range.h"
 
 namespace {
 
@@ -323,12 +324,14 @@ int64_t fsmc_gp_lml_max_rows(void) {   // the block column and the staged rows f
 fsmc_status fsmc_gp_lml(const double* theta, int64_t k, const double* d2, const double* y, int64_t n,
                         double jitter, int32_t residual, double* work, int64_t work_slots, double* lp,
                         void* stream_) {
+  FSMC_NVTX("fsmc_gp_lml");
   return fsmc_gp_lml_grad(theta, k, d2, y, n, jitter, residual, work, work_slots, lp, nullptr, stream_);
 }
 
 fsmc_status fsmc_gp_lml_grad(const double* theta, int64_t k, const double* d2, const double* y, int64_t n,
                              double jitter, int32_t residual, double* work, int64_t work_slots, double* lp,
                              double* grad, void* stream_) {
+  FSMC_NVTX("fsmc_gp_lml_grad");
   if (!theta || !d2 || !y || !work || !lp || k < 0 || n < 2 || work_slots < 1) {
     g_err = "gp_lml: bad arguments";
     return FSMC_ERR_ARG;

@@ -32,6 +32,7 @@
 
 #include "../../include/fsmc.h"
 #include "launch_count.h"
+#include "nvtx_range.h"
 
 namespace {
 
@@ -445,6 +446,7 @@ const char* fsmc_logreg_tc_last_error(void) { return g_err.c_str(); }
 fsmc_status fsmc_logreg_tc_eval2(const double* theta, int64_t k, void* theta_h16, const void* x_h16,
                                  const void* xt_h16, const double* xty, int64_t n_obs, int64_t dim, double* lp,
                                  double* grad, int32_t operand, void* stream_) {
+  FSMC_NVTX("fsmc_logreg_tc_eval2");
   if (dim != DF) { g_err = "fused logistic-regression kernel is compiled for d = 256"; return FSMC_ERR_UNSUPPORTED; }
   if (!theta || !theta_h16 || !x_h16 || !xt_h16 || !xty || !lp || !grad || k < 0 || n_obs < 1 ||
       (operand != 0 && operand != 1)) {

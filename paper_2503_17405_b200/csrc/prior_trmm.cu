@@ -27,6 +27,7 @@
 
 #include "../../include/fsmc.h"
 #include "launch_count.h"
+#include "nvtx_range.h"
 
 namespace {
 
@@ -155,6 +156,7 @@ const char* fsmc_prior_trmm_last_error(void) { return g_err.c_str(); }
 
 /* nu[r] = L nu[r] for k rows on the fp64 tensor cores (see the header). */
 fsmc_status fsmc_prior_trmm(const fsmc_target* t, double* nu, double* tmp, int64_t k, void* stream_) {
+  FSMC_NVTX("fsmc_prior_trmm");
   if (!t || !nu || !tmp || k < 0) { g_err = "prior_trmm needs a target, nu and tmp"; return FSMC_ERR_ARG; }
   if (t->prior_kind != FSMC_PRIOR_DENSE || !t->prior_t) {
     g_err = "prior_trmm needs a dense prior factor";
