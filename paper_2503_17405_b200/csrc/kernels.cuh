@@ -21,6 +21,12 @@ namespace fsmc {
 
 constexpr int kThreads = 128;
 
+// plain / amortized executor specialised per state for the compile-time
+// plugins (tick() VAR 2)
+#ifndef FSMC_VAR2
+#define FSMC_VAR2 1
+#endif
+
 // dynamic shared memory: one cooperative-normal scratch per warp, then the
 // per-group plugin scratch (dim doubles for dense operators plus whatever
 // the plugin asks for in fsmc_target.scratch, e.g. a GP kernel matrix)
@@ -525,8 +531,13 @@ struct Launch {
     return TK != 0 && p.variant == FSMC_BUNDLED && p.default_order;
   }
   static cudaError_t run(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
-    if constexpr (TK != 0)
+    if constexpr (TK != 0) {
       if (unrolled(p)) return persistent(fsm_run_kernel<F, G, E, TK, 1>, p, lc, s, 0, p.j_hi - p.j_lo);
+#if FSMC_VAR2
+      if (p.variant != FSMC_BUNDLED)
+        return persistent(fsm_run_kernel<F, G, E, TK, 2>, p, lc, s, 0, p.j_hi - p.j_lo);
+#endif
+    }
     return persistent(fsm_run_kernel<F, G, E, TK, 0>, p, lc, s, 0, p.j_hi - p.j_lo);
   }
   static cudaError_t profile(const Params& p, const LaunchCtx& lc, cudaStream_t s) {
