@@ -21,11 +21,6 @@ namespace fsmc {
 
 constexpr int kThreads = 128;
 
-// plain / amortized executor specialised per state for the compile-time
-// plugins (tick() VAR 2)
-#ifndef FSMC_VAR2
-#define FSMC_VAR2 1
-#endif
 
 // dynamic shared memory: one cooperative-normal scratch per warp, then the
 // per-group plugin scratch (dim doubles for dense operators plus whatever
