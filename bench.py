@@ -514,13 +514,16 @@ def main():
                       "launching stream)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs", "design_traffic": design}
     if draw_bytes:
-        tp = os.path.join(ROOT, "profiles", "r02_c2_traffic.json")
+        tp = os.path.join(ROOT, "profiles", "r06_c2_traffic.json")      # every launch at HEAD
+        if not os.path.exists(tp):
+            tp = os.path.join(ROOT, "profiles", "r02_c2_traffic.json")
         if os.path.exists(tp) and cfg.get("draw_window") in (3300, 4070):
-            # ncu DRAM bytes of one generator + window launch pair (draws + 4%:
-            # state and samples), scaled to this run by its draw bytes
+            # ncu DRAM bytes of the generator + window launches over a whole run, as a
+            # multiple of their draw bytes (0.95 at HEAD: some draws still in L2), scaled
+            # to this run by its draw bytes
             t = json.load(open(tp))
             roof["traffic"] = draw_bytes * t["measured_over_draw_bytes"]
-            roof["traffic_source"] = "profiles/r02_c2_traffic.json (per launch pair: %.0f MB measured, "\
+            roof["traffic_source"] = os.path.relpath(tp, ROOT) + " (per launch pair: %.0f MB measured, "\
                 "%.0f MB of draws)" % (t["measured_per_launch_pair"] / 1e6,
                                       t["algorithmic_draw_bytes_per_launch_pair"] / 1e6)
     tp3 = os.path.join(ROOT, "profiles", "r03_c3_traffic.json")
