@@ -526,12 +526,14 @@ def main():
             roof["traffic_source"] = os.path.relpath(tp, ROOT) + " (per launch pair: %.0f MB measured, "\
                 "%.0f MB of draws)" % (t["measured_per_launch_pair"] / 1e6,
                                       t["algorithmic_draw_bytes_per_launch_pair"] / 1e6)
-    tp3 = os.path.join(ROOT, "profiles", "r03_c3_traffic.json")
+    tp3 = os.path.join(ROOT, "profiles", "r06_c3_traffic.json")     # every launch at HEAD
+    if not os.path.exists(tp3):
+        tp3 = os.path.join(ROOT, "profiles", "r03_c3_traffic.json")
     if cfg["family"] == "nuts" and not cfg.get("batched") and d == 100 and os.path.exists(tp3):
         # ncu DRAM bytes per chain-sample of the C3 run kernel, scaled to this run
         t = json.load(open(tp3))
         roof["traffic"] = t["measured_bytes_per_chain_sample"] * n * m
-        roof["traffic_source"] = "profiles/r03_c3_traffic.json (%.0f B per chain-sample measured)" \
+        roof["traffic_source"] = os.path.relpath(tp3, ROOT) + " (%.0f B per chain-sample measured)" \
             % t["measured_bytes_per_chain_sample"]
     if cfg["family"] == "drmh" and proposals:
         # executed fp64 flops per DRMH proposal (DFMA = 2), from ncu SASS counts of
