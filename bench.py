@@ -507,7 +507,10 @@ def main():
     roof = {"bound": "hbm", "achieved": sm_ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": sm_ach / peaks["hbm_gbs"], "traffic": None,
             "kernel": ("drmh_draws_ilp_kernel<4> + fsm_window_kernel<DrmhWX,1,10,MOG,1>" if win else
-                       "fsm_run_kernel<Drmh>" if cfg["family"] == "drmh" else "fsm_run_kernel"),
+                       "fsm_advance_kernel<Ess> rounds + prior_trmm_kernel (DMMA nu = L eps), every "
+                       "launch of the run" if cfg.get("prior_transform") else
+                       "fsm_run_kernel<%s>" % {"drmh": "Drmh", "ess": "Ess", "nuts": "Nuts"}.get(
+                           cfg["family"], cfg["family"])),
             "kernel_ms": kms, "unit_of_work": uname, "units": units, "bytes_per_unit": per_unit,
             "algorithmic_bytes": units * per_unit,
             "source": "SURVEY.md 8(d) per-unit bytes x units / kernel time (CUDA events on the "
@@ -534,6 +537,13 @@ def main():
         t = json.load(open(tp3))
         roof["traffic"] = t["measured_bytes_per_chain_sample"] * n * m
         roof["traffic_source"] = os.path.relpath(tp3, ROOT) + " (%.0f B per chain-sample measured)" \
+            % t["measured_bytes_per_chain_sample"]
+    tpc = os.path.join(ROOT, "profiles", "r06_%s_traffic.json" % args.config)
+    if roof["traffic"] is None and not cfg.get("batched") and os.path.exists(tpc):
+        # ncu DRAM bytes of every launch of the run's kernels per chain-sample, scaled
+        t = json.load(open(tpc))
+        roof["traffic"] = t["measured_bytes_per_chain_sample"] * n * m
+        roof["traffic_source"] = os.path.relpath(tpc, ROOT) + " (%.0f B per chain-sample measured)" \
             % t["measured_bytes_per_chain_sample"]
     if cfg["family"] == "drmh" and proposals:
         # executed fp64 flops per DRMH proposal (DFMA = 2), from ncu SASS counts of
